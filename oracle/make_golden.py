@@ -1,0 +1,136 @@
+"""TEST INFRASTRUCTURE ONLY — generate tests/golden/*.npz from the REAL reference.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python oracle/make_golden.py
+
+It imports the reference package ``vkt`` read-only and records, for a matrix
+of small seeded volumes, the reference's own outputs:
+  * clamp cases: ``vkt.apply_filter`` verbatim (filters.py:69-95);
+  * wrap / mirror / border cases: the reference-anchored construction of
+    SURVEY.md §8(c) — pad the stored cells with np.pad(mode), run the
+    reference apply_filter on the padded volume, crop the centre;
+  * fill cases: ``vkt.fill_range`` (core.py:39-55).
+The fixtures are committed; the GPU box never needs /root/reference.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+OUT = ROOT / "tests" / "golden"
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import vkt  # noqa: E402  (the reference, read-only)
+from vkt.ops.filters import box_kernel  # noqa: E402
+
+FMTS = {1: vkt.DataFormat.UINT8, 2: vkt.DataFormat.UINT16, 3: vkt.DataFormat.FLOAT32}
+PAD = {"wrap": "wrap", "mirror": "symmetric", "border": "constant"}
+
+
+def random_stored(rng, dims, fmt):
+    nx, ny, nz = dims
+    if fmt == 3:
+        return rng.random((nz, ny, nx), dtype=np.float32)
+    dt = np.uint8 if fmt == 1 else np.uint16
+    return rng.integers(0, np.iinfo(dt).max + 1, size=(nz, ny, nx), dtype=dt)
+
+
+def reference_filter(stored, fmt, mapping, kernel, mode):
+    nz, ny, nx = stored.shape
+    if mode == "clamp":
+        v = vkt.StructuredVolume((nx, ny, nz), FMTS[fmt], (1, 1, 1), mapping)
+        v.array()[...] = stored
+        vkt.apply_filter(v, kernel)
+        return v.array().copy()
+    r = kernel.radius
+    p = np.pad(stored, ((r.z, r.z), (r.y, r.y), (r.x, r.x)), mode=PAD[mode])
+    big = vkt.StructuredVolume(p.shape[::-1], FMTS[fmt], (1, 1, 1), mapping)
+    big.array()[...] = p
+    vkt.apply_filter(big, kernel)
+    return big.array()[r.z:r.z + nz, r.y:r.y + ny, r.x:r.x + nx].copy()
+
+
+def kernels(rng):
+    aniso = rng.normal(size=15)
+    yield "gauss3", vkt.gaussian_kernel(1.0, 3)
+    yield "gauss5", vkt.gaussian_kernel(1.0)
+    yield "gauss7", vkt.gaussian_kernel(1.5)
+    yield "box5", box_kernel(5)
+    lap = np.zeros((3, 3, 3))
+    lap[1, 1, 1] = -6.0
+    for z, y, x in ((0, 1, 1), (2, 1, 1), (1, 0, 1), (1, 2, 1), (1, 1, 0), (1, 1, 2)):
+        lap[z, y, x] = 1.0
+    yield "lap3", vkt.Kernel((3, 3, 3), lap)
+    yield "aniso315", vkt.Kernel((3, 1, 5), aniso / np.abs(aniso).sum())
+    yield "ident1", vkt.Kernel((1, 1, 1), [1.0])
+    yield "rand3", vkt.Kernel((3, 3, 3), rng.normal(size=27) * 0.2)
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    rng = np.random.default_rng(20220321)
+    cases = {}
+    idx = 0
+    shapes = [(13, 11, 9), (6, 5, 7), (2, 3, 4), (1, 1, 5), (17, 4, 3)]
+    for kname, kernel in kernels(rng):
+        for fmt in (1, 2, 3):
+            mappings = [(0.0, 1.0)] if fmt == 3 else [(0.0, 1.0), (-1.0, 3.0)]
+            for mapping in mappings:
+                for mode in ("clamp", "wrap", "mirror", "border"):
+                    dims = shapes[idx % len(shapes)]
+                    idx += 1
+                    stored = random_stored(rng, dims, fmt)
+                    out = reference_filter(stored, fmt, mapping, kernel, mode)
+                    key = f"c{idx:04d}"
+                    cases[f"{key}/input"] = stored
+                    cases[f"{key}/output"] = out
+                    cases[f"{key}/weights"] = kernel.weights
+                    cases[f"{key}/meta"] = np.array(
+                        [fmt, mapping[0], mapping[1], ("wrap", "mirror", "clamp", "border").index(mode)],
+                        dtype=np.float64)
+                    cases[f"{key}/name"] = np.array(f"{kname}/{FMTS[fmt].short_name}/{mapping}/{mode}")
+    np.savez_compressed(OUT / "filter_cases.npz", **cases)
+
+    # bench-shaped fixture: the reference generator at seed 7 (bench.py:38-48)
+    # on a 24^3 u8 cube through gaussian_kernel(1.0, 3), the bench's kernel (bench.py:97)
+    v = vkt.synthetic_structured(24, vkt.DataFormat.UINT8, 7)
+    before = v.array().copy()
+    vkt.apply_filter(v, vkt.gaussian_kernel(1.0, 3))
+    np.savez_compressed(OUT / "bench_case.npz", input=before, output=v.array().copy())
+
+    # fill cases (core.py:39-55): (dims, fmt, mapping, roi lower, roi upper, value)
+    fills = {}
+    frng = np.random.default_rng(99)
+    specs = [
+        ((64, 64, 64), 1, (0.0, 1.0), (1, 1, 1), (63, 63, 63), 1.0),   # Fig. 4 session
+        ((8, 8, 8), 1, (0.0, 1.0), (0, 0, 0), (8, 8, 8), 0.5),
+        ((6, 6, 6), 1, (0.0, 1.0), (1, 2, 3), (4, 5, 6), 0.25),
+        ((4, 4, 4), 1, (0.0, 1.0), (-5, -5, -5), (99, 99, 99), 1.0),
+        ((9, 7, 5), 2, (-1.0, 3.0), (2, 0, 1), (9, 7, 4), 0.3337),
+        ((9, 7, 5), 3, (0.0, 1.0), (3, 1, 0), (7, 6, 5), -2.5),
+        ((33, 5, 4), 1, (0.0, 1.0), (1, 1, 1), (32, 4, 3), 0.7),
+        ((33, 5, 4), 2, (0.0, 1.0), (0, 0, 0), (33, 5, 4), 2.0),
+        ((4, 4, 4), 2, (0.0, 1.0), (2, 2, 2), (2, 2, 2), 1.0),          # empty roi
+        ((31, 3, 2), 3, (0.0, 1.0), (5, 0, 0), (31, 3, 2), 0.1),
+    ]
+    for i, (dims, fmt, mapping, lower, upper, value) in enumerate(specs):
+        stored = random_stored(frng, dims, fmt)
+        if i == 0:  # the Fig. 4 session starts from a zero-filled volume
+            stored = np.zeros_like(stored)
+        v = vkt.StructuredVolume(dims, FMTS[fmt], (1, 1, 1), mapping)
+        v.array()[...] = stored
+        vkt.fill_range(v, vkt.box3i(lower, upper), value)
+        fills[f"f{i:02d}/input"] = stored
+        fills[f"f{i:02d}/output"] = v.array().copy()
+        fills[f"f{i:02d}/spec"] = np.array([fmt, mapping[0], mapping[1], *lower, *upper, value])
+    np.savez_compressed(OUT / "fill_cases.npz", **fills)
+    print(f"wrote {idx} filter cases, {len(specs)} fill cases to {OUT}")
+
+
+if __name__ == "__main__":
+    main()

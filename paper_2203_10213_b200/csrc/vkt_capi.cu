@@ -1,0 +1,174 @@
+// vkt_capi.cu — the extern "C" boundary declared in include/vkt_b200.h.
+//
+// Validation mirrors the reference's error contract:
+//   even / non-positive kernel extents -> EvenKernelDims   (filters.py:32-33)
+//   non-finite weights                 -> InvalidArgument  (filters.py:37-38)
+//   dims < 1, degenerate mapping       -> InvalidArgument  (volume.py:133-134, 80-81)
+//   device allocation failure          -> AllocationFailure (managed.py:45-49)
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "dispatch.h"
+
+namespace vkt {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local char g_detail[512] = "";
+
+void set_error_detail(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_detail, sizeof(g_detail), fmt, ap);
+  va_end(ap);
+}
+
+static int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_detail, sizeof(g_detail), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
+  if (a == nullptr) return fail(VKT_INVALID_ARGUMENT, "args is NULL");
+  if (a->kdims.x < 1 || a->kdims.y < 1 || a->kdims.z < 1 || a->kdims.x % 2 == 0 ||
+      a->kdims.y % 2 == 0 || a->kdims.z % 2 == 0)
+    return fail(VKT_EVEN_KERNEL_DIMS, "kernel dims must be odd, got (%d, %d, %d)", a->kdims.x,
+                a->kdims.y, a->kdims.z);
+  if (a->dims.x < 1 || a->dims.y < 1 || a->dims.z < 1)
+    return fail(VKT_INVALID_ARGUMENT, "dims must be >= 1 per axis, got (%d, %d, %d)", a->dims.x,
+                a->dims.y, a->dims.z);
+  if (a->format != VKT_U8 && a->format != VKT_U16 && a->format != VKT_F32)
+    return fail(VKT_INVALID_ARGUMENT, "unknown data format code %d", a->format);
+  if (a->address_mode < VKT_WRAP || a->address_mode > VKT_BORDER)
+    return fail(VKT_INVALID_ARGUMENT, "unknown address mode %d", a->address_mode);
+  if (a->src == nullptr || a->dst == nullptr || a->weights == nullptr)
+    return fail(VKT_INVALID_ARGUMENT, "src, dst and weights must be non-NULL");
+  if (a->src == a->dst)
+    return fail(VKT_INVALID_ARGUMENT, "dst must not alias src (the filter reads a snapshot)");
+  if (!(std::isfinite(a->map_lo) && std::isfinite(a->map_hi)) || !(a->map_lo < a->map_hi))
+    return fail(VKT_INVALID_ARGUMENT, "voxel mapping needs finite lo < hi, got [%g, %g]",
+                a->map_lo, a->map_hi);
+
+  const size_t ntaps = (size_t)a->kdims.x * a->kdims.y * a->kdims.z;
+  plan.args = a;
+  plan.w32.resize(ntaps);
+  double sum = 0.0;
+  for (size_t i = 0; i < ntaps; ++i) {
+    double w = a->weights[i];
+    if (!std::isfinite(w)) return fail(VKT_INVALID_ARGUMENT, "kernel weights must be finite");
+    plan.w32[i] = (float)w;
+    sum += w;
+  }
+  plan.sum_w = sum;
+  if (a->format == VKT_F32) {
+    plan.epi_c = 0.0f;
+  } else {
+    const double mx = a->format == VKT_U8 ? 255.0 : 65535.0;
+    plan.epi_c = (float)(a->map_lo * (sum - 1.0) / (a->map_hi - a->map_lo) * mx);
+  }
+
+  const int64_t gnz = a->global_nz > 0 ? a->global_nz : a->dims.z;
+  if (a->z_offset < 0 || a->z_offset + a->dims.z > gnz)
+    return fail(VKT_INVALID_ARGUMENT, "slab [%lld, %lld) outside global z extent %lld",
+                (long long)a->z_offset, (long long)(a->z_offset + a->dims.z), (long long)gnz);
+  plan.z_begin = a->out_z_begin > 0 ? a->out_z_begin : 0;
+  plan.z_end = a->out_z_end > 0 ? (a->out_z_end < a->dims.z ? a->out_z_end : a->dims.z) : a->dims.z;
+
+  const int rz = a->kdims.z / 2;
+  SlabGeom& g = plan.geom;
+  g.src = a->src;
+  g.halo_lo = a->halo_lo;
+  g.halo_hi = a->halo_hi;
+  g.plane_elems = (int64_t)a->dims.x * a->dims.y;
+  g.nz = a->dims.z;
+  g.rz = rz;
+  g.z_offset = a->z_offset;
+  g.global_nz = gnz;
+
+  // Without halos every z tap must resolve inside the slab (unsharded volume,
+  // or a shard whose neighbours' planes are not needed).
+  if (rz > 0 && (a->halo_lo == nullptr || a->halo_hi == nullptr) && gnz != a->dims.z)
+    return fail(VKT_INVALID_ARGUMENT,
+                "sharded slab (global_nz=%lld, local nz=%d) needs halo_lo and halo_hi",
+                (long long)gnz, a->dims.z);
+
+  if (a->flags & VKT_FLAG_EXACT_F64) plan.path = VKT_PATH_EXACT;
+  else if (!(a->flags & VKT_FLAG_FORCE_DIRECT) && tma_supported(*a)) plan.path = VKT_PATH_TMA;
+  else plan.path = VKT_PATH_DIRECT;
+  return VKT_OK;
+}
+
+}  // namespace vkt
+
+using namespace vkt;
+
+extern "C" {
+
+int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
+  FilterPlan plan;
+  int st = validate_and_plan(args, plan);
+  if (st != VKT_OK) return st;
+  if (plan.z_end <= plan.z_begin) return VKT_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (plan.path == VKT_PATH_TMA) {
+    st = launch_filter_tma(plan, s);
+    if (st != -1) return st;
+    plan.path = VKT_PATH_DIRECT;
+  }
+  return launch_filter_direct(plan, s);
+}
+
+int vkt_filter_path(const vkt_filter_args* args) {
+  FilterPlan plan;
+  if (validate_and_plan(args, plan) != VKT_OK) return VKT_PATH_NONE;
+  return plan.path;
+}
+
+int vkt_fill_box(void* dst, vkt_int3 dims, int32_t format, vkt_int3 lo, vkt_int3 hi,
+                 uint32_t stored_bits, vkt_stream_t stream) {
+  if (dst == nullptr) return fail(VKT_INVALID_ARGUMENT, "dst is NULL");
+  if (dims.x < 1 || dims.y < 1 || dims.z < 1)
+    return fail(VKT_INVALID_ARGUMENT, "dims must be >= 1 per axis");
+  if (format != VKT_U8 && format != VKT_U16 && format != VKT_F32)
+    return fail(VKT_INVALID_ARGUMENT, "unknown data format code %d", format);
+  return launch_fill_box(dst, dims, format, lo, hi, stored_bits,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int vkt_fill_synthetic(void* dst, vkt_int3 dims, int32_t format, uint64_t seed, int64_t z_offset,
+                       vkt_stream_t stream) {
+  if (dst == nullptr) return fail(VKT_INVALID_ARGUMENT, "dst is NULL");
+  if (dims.x < 1 || dims.y < 1 || dims.z < 1)
+    return fail(VKT_INVALID_ARGUMENT, "dims must be >= 1 per axis");
+  if (format != VKT_U8 && format != VKT_U16 && format != VKT_F32)
+    return fail(VKT_INVALID_ARGUMENT, "unknown data format code %d", format);
+  return launch_fill_synthetic(dst, dims, format, seed, z_offset,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+const char* vkt_status_name(int status) {
+  switch (status) {
+    case VKT_OK: return "OK";
+    case VKT_INVALID_ARGUMENT: return "InvalidArgument";
+    case VKT_EVEN_KERNEL_DIMS: return "EvenKernelDims";
+    case VKT_ALLOCATION_FAILURE: return "AllocationFailure";
+    case VKT_DEVICE_FAILURE: return "DeviceFailure";
+    default: return "Unknown";
+  }
+}
+
+const char* vkt_last_error_detail(void) { return g_detail; }
+
+uint64_t vkt_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int vkt_abi_version(void) { return 10000; }
+
+}  // extern "C"

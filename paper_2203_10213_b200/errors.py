@@ -1,0 +1,57 @@
+"""Error contract of the drop-in.
+
+The reference identifies failures by exception class name across process and
+language boundaries (``VktError.name``, pkg/src/vkt/errors.py:9-14).  The
+classes the ApplyFilter / Fill path can raise keep those names; the C ABI's
+status codes map onto them through ``vkt_status_name`` (include/vkt_b200.h).
+"""
+
+from __future__ import annotations
+
+
+class VktError(Exception):
+    """Root of every error this package raises; ``name`` is the class name."""
+
+    @property
+    def name(self) -> str:
+        return self.__class__.__name__
+
+
+class InvalidArgument(VktError):
+    """A documented precondition does not hold (errors.py:17)."""
+
+
+class IndexOutOfRange(VktError):
+    """Cell index outside the volume (errors.py:21)."""
+
+
+class AllocationFailure(VktError):
+    """Device memory cannot hold the requested bytes (errors.py:25)."""
+
+
+class EvenKernelDims(VktError):
+    """Kernel extents must be odd on every axis (errors.py:53)."""
+
+
+class DimsMismatch(VktError):
+    """Operand volumes disagree in dimensions, format or mapping (errors.py:49)."""
+
+
+class DeviceFailure(VktError):
+    """The CUDA runtime reported an error, or no CUDA device / library exists.
+
+    New in this package: the reference has no accelerator (its "device" is
+    an emulated arena, managed.py:31-59), so it never raises this.
+    """
+
+
+_BY_NAME = {
+    cls.__name__: cls
+    for cls in (InvalidArgument, IndexOutOfRange, AllocationFailure, EvenKernelDims,
+                DimsMismatch, DeviceFailure)
+}
+
+
+def from_status_name(name: str, detail: str) -> VktError:
+    """Exception instance for a C-ABI status name (``vkt_status_name``)."""
+    return _BY_NAME.get(name, DeviceFailure)(detail)

@@ -1,0 +1,232 @@
+"""ApplyFilter: 3D correlation of a StructuredVolume on the B200.
+
+Reference: ``apply_filter(volume, kernel)`` (pkg/src/vkt/ops/filters.py:69-95)
+correlates (no kernel flip) in mapped-value space against an immutable
+snapshot with clamp-to-edge reads and re-quantizes in place.  This module
+keeps that call and its ``Kernel`` / ``gaussian_kernel`` / ``box_kernel``
+helpers (filters.py:23-66) and adds the north star's
+``ApplyFilter(dst, src, filter, address_mode)`` with the Wrap / Mirror /
+Clamp / Border modes.  All arithmetic happens in ``libvkt_b200.so``
+(include/vkt_b200.h); this file only validates, packs arguments and picks
+the stream.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from enum import IntEnum
+
+import numpy as np
+
+from . import _capi
+from .errors import EvenKernelDims, InvalidArgument
+from .execution import FilterPath, debug, get_execution_policy, timed
+from .geom import Vec3i, ivec3
+from .volume import DataFormat, StructuredVolume, require_same_layout
+
+
+class AddressMode(IntEnum):
+    """Boundary handling; values match VKT_WRAP.. in include/vkt_b200.h."""
+
+    WRAP = 0     # i mod n                      (np.pad "wrap")
+    MIRROR = 1   # edge-duplicating reflection  (np.pad "symmetric")
+    CLAMP = 2    # clamp-to-edge: the reference (np.pad "edge", filters.py:78)
+    BORDER = 3   # stored value 0               (np.pad "constant")
+
+    @classmethod
+    def coerce(cls, v) -> "AddressMode":
+        if isinstance(v, AddressMode):
+            return v
+        if isinstance(v, str):
+            try:
+                return cls[v.strip().upper()]
+            except KeyError:
+                raise InvalidArgument(f"unknown address mode {v!r}") from None
+        try:
+            return cls(int(v))
+        except ValueError:
+            raise InvalidArgument(f"unknown address mode {v!r}") from None
+
+
+class Kernel:
+    """Dense correlation kernel with odd extent per axis (filters.py:23-43).
+
+    ``weights`` is float64 shaped (kz, ky, kx), built from an x-fastest flat
+    sequence exactly like the reference's reshape (filters.py:34-36).
+    """
+
+    def __init__(self, dims, weights):
+        self.dims = ivec3(dims, "kernel dims")
+        if any(d < 1 or d % 2 == 0 for d in self.dims):
+            raise EvenKernelDims(f"kernel dims must be odd, got {tuple(self.dims)}")
+        try:
+            w = np.asarray(weights, dtype=np.float64).reshape(self.dims.z, self.dims.y, self.dims.x)
+        except ValueError as e:
+            raise InvalidArgument(f"kernel weights do not match dims {tuple(self.dims)}: {e}") from None
+        if not np.isfinite(w).all():
+            raise InvalidArgument("kernel weights must be finite")
+        self.weights = w
+
+    @property
+    def radius(self) -> Vec3i:
+        d = self.dims
+        return Vec3i(d.x // 2, d.y // 2, d.z // 2)
+
+    @property
+    def tap_count(self) -> int:
+        d = self.dims
+        return d.x * d.y * d.z
+
+    def __repr__(self):
+        return f"Kernel(dims={tuple(self.dims)})"
+
+
+#: The north star calls the kernel a Filter; same type.
+Filter = Kernel
+
+
+def gaussian_kernel(sigma: float, size: int | None = None) -> Kernel:
+    """Normalized isotropic Gaussian (filters.py:46-59).
+
+    Same float64 operation sequence as the reference so the weights are
+    bit-identical: separable exp profile, outer product (z, y, x), divided by
+    the numpy sum.  Default extent 2*ceil(2*sigma)+1.
+    """
+    if not sigma > 0:
+        raise InvalidArgument(f"sigma must be > 0, got {sigma}")
+    if size is None:
+        size = 2 * int(math.ceil(2.0 * sigma)) + 1
+    if size % 2 == 0:
+        raise EvenKernelDims(f"kernel size must be odd, got {size}")
+    r = size // 2
+    t = np.arange(-r, r + 1, dtype=np.float64)
+    prof = np.exp(-0.5 * (t / sigma) ** 2)
+    w = prof[:, None, None] * prof[None, :, None] * prof[None, None, :]
+    w /= w.sum()
+    return Kernel((size, size, size), w)
+
+
+def box_kernel(size: int) -> Kernel:
+    """Uniform kernel 1/size^3 (filters.py:62-66)."""
+    if size % 2 == 0:
+        raise EvenKernelDims(f"kernel size must be odd, got {size}")
+    return Kernel((size, size, size), np.full((size, size, size), 1.0 / size**3))
+
+
+def laplacian_kernel() -> Kernel:
+    """7-point Laplacian in a dense 3^3 footprint (centre -6, faces +1).
+
+    Not in the reference; BASELINE config 4 uses it.  All 27 taps are
+    evaluated, like the reference would.
+    """
+    w = np.zeros((3, 3, 3))
+    w[1, 1, 1] = -6.0
+    for z, y, x in ((0, 1, 1), (2, 1, 1), (1, 0, 1), (1, 2, 1), (1, 1, 0), (1, 1, 2)):
+        w[z, y, x] = 1.0
+    return Kernel((3, 3, 3), w)
+
+
+def _flags(policy) -> int:
+    if policy.filter_path is FilterPath.EXACT:
+        return _capi.FLAG_EXACT_F64
+    if policy.filter_path is FilterPath.DIRECT:
+        return _capi.FLAG_FORCE_DIRECT
+    return 0
+
+
+def make_args(dst_ptr: int, src_ptr: int, dims, fmt: DataFormat, mapping, kernel: Kernel,
+              mode: AddressMode, *, halo_lo: int = 0, halo_hi: int = 0, z_offset: int = 0,
+              global_nz: int = 0, out_z_begin: int = 0, out_z_end: int = 0,
+              flags: int = 0):
+    """Pack a ``vkt_filter_args``; returns (args, keepalive) — keep both alive."""
+    w = np.ascontiguousarray(kernel.weights.reshape(-1), dtype=np.float64)
+    a = _capi.FilterArgs()
+    a.src = src_ptr
+    a.dst = dst_ptr
+    a.dims = _capi.int3(dims)
+    a.format = fmt.value
+    a.map_lo, a.map_hi = float(mapping[0]), float(mapping[1])
+    a.weights = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    a.kdims = _capi.int3(kernel.dims)
+    a.address_mode = int(mode)
+    a.halo_lo = halo_lo or None
+    a.halo_hi = halo_hi or None
+    a.z_offset = int(z_offset)
+    a.global_nz = int(global_nz)
+    a.out_z_begin = int(out_z_begin)
+    a.out_z_end = int(out_z_end)
+    a.flags = int(flags)
+    return a, w
+
+
+def launch(args, stream_handle: int) -> None:
+    """Call ``vkt_apply_filter`` and raise the reference-named error on failure."""
+    lib = _capi.load()
+    _capi.check(lib.vkt_apply_filter(ctypes.byref(args), ctypes.c_void_p(stream_handle)))
+
+
+def filter_path(dst: StructuredVolume, src: StructuredVolume, kernel: Kernel,
+                address_mode=AddressMode.CLAMP) -> str:
+    """Which kernel ApplyFilter would launch ("tma", "direct", "exact")."""
+    mode = AddressMode.coerce(address_mode)
+    args, _keep = make_args(dst.data_ptr(), src.data_ptr(), src.dims, src.format, src.mapping,
+                            kernel, mode, flags=_flags(get_execution_policy()))
+    return _capi.PATH_NAMES[_capi.load().vkt_filter_path(ctypes.byref(args))]
+
+
+def _current_stream(volume: StructuredVolume) -> int:
+    import torch
+
+    return int(torch.cuda.current_stream(volume.data.device).cuda_stream)
+
+
+@timed("ApplyFilter")
+def ApplyFilter(dst: StructuredVolume, src: StructuredVolume, filter: Kernel,
+                address_mode=AddressMode.CLAMP) -> None:
+    """dst = correlate(src, filter) under ``address_mode``, re-quantized to dst's format.
+
+    ``dst`` and ``src`` must agree in dims, format and mapping.  Passing the
+    same volume twice filters in place (snapshot semantics, filters.py:77).
+    Asynchronous on the current torch CUDA stream.
+    """
+    if not isinstance(filter, Kernel):
+        raise InvalidArgument("filter must be a Kernel/Filter")
+    mode = AddressMode.coerce(address_mode)
+    if dst is src:
+        _apply_in_place(src, filter, mode)
+        return
+    require_same_layout(dst, src)
+    policy = get_execution_policy()
+    args, _keep = make_args(dst.data_ptr(), src.data_ptr(), src.dims, src.format, src.mapping,
+                            filter, mode, flags=_flags(policy))
+    debug(f"ApplyFilter {src!r} k={tuple(filter.dims)} mode={mode.name}")
+    launch(args, _current_stream(src))
+
+
+def _apply_in_place(volume: StructuredVolume, kernel: Kernel, mode: AddressMode) -> None:
+    from .volume import DeviceBuffer
+
+    out = StructuredVolume(volume.dims, volume.format, volume.cell_size, volume.mapping,
+                           data=DeviceBuffer(volume.nbytes, device=volume.data.device, zero=False))
+    args, _keep = make_args(out.data_ptr(), volume.data_ptr(), volume.dims, volume.format,
+                            volume.mapping, kernel, mode, flags=_flags(get_execution_policy()))
+    import torch
+
+    stream = torch.cuda.current_stream(volume.data.device)
+    launch(args, int(stream.cuda_stream))
+    # The old buffer goes back to the torch caching allocator; recording the
+    # launch stream keeps it from being reused before the kernel has read it.
+    volume.data.tensor.record_stream(stream)
+    volume.swap_storage(out)
+
+
+@timed("ApplyFilter")
+def apply_filter(volume: StructuredVolume, kernel: Kernel, address_mode=AddressMode.CLAMP) -> None:
+    """In-place filter with the reference's signature (filters.py:69-95).
+
+    The reference always clamps; ``address_mode`` is an optional extension.
+    """
+    if not isinstance(kernel, Kernel):
+        raise InvalidArgument("kernel must be a Kernel")
+    _apply_in_place(volume, kernel, AddressMode.coerce(address_mode))

@@ -146,7 +146,8 @@ def make_args(dst_ptr: int, src_ptr: int, dims, fmt: DataFormat, mapping, kernel
     a.dst = dst_ptr
     a.dims = _capi.int3(dims)
     a.format = fmt.value
-    a.map_lo, a.map_hi = float(mapping[0]), float(mapping[1])
+    lo, hi = mapping
+    a.map_lo, a.map_hi = float(lo), float(hi)
     a.weights = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     a.kdims = _capi.int3(kernel.dims)
     a.address_mode = int(mode)

@@ -1,12 +1,145 @@
-// filter_tma.cu — tiled sm_100a ApplyFilter kernel (TMA plane pipeline).
-// Placeholder: the tiled kernel lands in the next commit.
-#include "common.cuh"
+// filter_tma.cu — host side of the tiled TMA ApplyFilter kernel: eligibility,
+// tensor-map encoding (driver entry point, no libcuda link), chunk sizing and
+// dispatch.  The kernels are instantiated per voxel format in
+// filter_tma_{u8,u16,f32}.cu so the 36 specialisations compile in parallel.
+#include <cuda.h>
+
+#include <mutex>
+
 #include "dispatch.h"
+#include "filter_tma.cuh"
 
 namespace vkt {
+namespace tma {
+template <typename T>
+cudaError_t launch_tma_dtype(int k, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
+                             const CUtensorMap& mh, const TmaParams& p, const float* w32, dim3 grid,
+                             cudaStream_t s);
+extern template cudaError_t launch_tma_dtype<uint8_t>(int, int, const CUtensorMap&,
+                                                      const CUtensorMap&, const CUtensorMap&,
+                                                      const TmaParams&, const float*, dim3,
+                                                      cudaStream_t);
+extern template cudaError_t launch_tma_dtype<uint16_t>(int, int, const CUtensorMap&,
+                                                       const CUtensorMap&, const CUtensorMap&,
+                                                       const TmaParams&, const float*, dim3,
+                                                       cudaStream_t);
+extern template cudaError_t launch_tma_dtype<float>(int, int, const CUtensorMap&,
+                                                    const CUtensorMap&, const CUtensorMap&,
+                                                    const TmaParams&, const float*, dim3,
+                                                    cudaStream_t);
+}  // namespace tma
 
-bool tma_supported(const vkt_filter_args&) { return false; }
+namespace {
 
-int launch_filter_tma(const FilterPlan&, cudaStream_t) { return -1; }
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int bpc_of(int format) { return format == VKT_U8 ? 1 : format == VKT_U16 ? 2 : 4; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int r) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return false;
+  const int bpc = bpc_of(format);
+  CUtensorMapDataType dt = format == VKT_U8    ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                           : format == VKT_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)nx * bpc, (cuuint64_t)nx * ny * bpc};
+  cuuint32_t box[3] = {(cuuint32_t)tma::box_width(r, bpc), (cuuint32_t)(tma::TY + 2 * r), 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult res = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool tma_supported(const vkt_filter_args& a) {
+  if (a.flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
+  const int k = a.kdims.x;
+  if (a.kdims.y != k || a.kdims.z != k) return false;
+  if (k != 3 && k != 5 && k != 7) return false;
+  const int bpc = bpc_of(a.format);
+  if (((int64_t)a.dims.x * bpc) % 16 != 0) return false;  // TMA global stride rule
+  if (!aligned16(a.src) || !aligned16(a.dst)) return false;
+  if (a.halo_lo && !aligned16(a.halo_lo)) return false;
+  if (a.halo_hi && !aligned16(a.halo_hi)) return false;
+  return encode_fn() != nullptr;
+}
+
+int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
+  const vkt_filter_args& a = *plan.args;
+  const int k = a.kdims.x, r = k / 2;
+  CUtensorMap ms, ml, mh;
+  if (!encode(&ms, a.src, a.format, a.dims.x, a.dims.y, a.dims.z, r)) return -1;
+  ml = ms;
+  mh = ms;
+  if (a.halo_lo && r > 0 && !encode(&ml, a.halo_lo, a.format, a.dims.x, a.dims.y, r, r)) return -1;
+  if (a.halo_hi && r > 0 && !encode(&mh, a.halo_hi, a.format, a.dims.x, a.dims.y, r, r)) return -1;
+
+  tma::TmaParams p{};
+  p.dst = a.dst;
+  p.src = a.src;
+  p.halo_lo = a.halo_lo;
+  p.halo_hi = a.halo_hi;
+  p.nx = a.dims.x;
+  p.ny = a.dims.y;
+  p.nz = a.dims.z;
+  p.z_begin = plan.z_begin;
+  p.z_end = plan.z_end;
+  p.z_offset = plan.geom.z_offset;
+  p.global_nz = plan.geom.global_nz;
+  p.c = plan.epi_c;
+
+  // Chunk depth: long enough to amortise the 2R-plane z halo of a chunk,
+  // short enough for >= ~8 CTAs per SM worth of work items (tail effect).
+  const int nzo = plan.z_end - plan.z_begin;
+  const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
+  int zc = 64;
+  while (zc > 8 && nxy * ((nzo + zc - 1) / zc) < 148 * 8) zc /= 2;
+  if (zc > nzo) zc = nzo;
+  p.zc = zc;
+  dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + tma::TY - 1) / tma::TY,
+            (nzo + zc - 1) / zc);
+  if (grid.y > 65535 || grid.z > 65535) return -1;
+
+  cudaError_t err;
+  switch (a.format) {
+    case VKT_U8:
+      err = tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      break;
+    case VKT_U16:
+      err = tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      break;
+    default:
+      err = tma::launch_tma_dtype<float>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      break;
+  }
+  count_launch();
+  if (err != cudaSuccess) {
+    set_error_detail("filter_tma launch: %s", cudaGetErrorString(err));
+    return VKT_DEVICE_FAILURE;
+  }
+  return VKT_OK;
+}
 
 }  // namespace vkt

@@ -38,16 +38,29 @@ constexpr int XPT = 4;     // outputs per thread in x
 constexpr int THREADS = (TX / XPT) * TY;  // 256
 constexpr int STAGES = 4;
 
+// Box geometry shared by the host (tensor-map encode) and the kernel.
+__host__ __device__ constexpr int box_align_left(int r, int bpc) {
+  return (r + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
+}
+__host__ __device__ constexpr int box_width(int r, int bpc) {
+  return (box_align_left(r, bpc) + TX + r + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
+}
+
 template <typename T, int R>
 struct Geo {
-  static constexpr int ALIGN_ELEMS = 16 / (int)sizeof(T);
-  static constexpr int W = TX + 2 * R;  // needed box width
-  static constexpr int BX = (W + ALIGN_ELEMS - 1) / ALIGN_ELEMS * ALIGN_ELEMS;
+  // TMA needs the innermost box coordinate at a 16-byte multiple (measured:
+  // tools/tma_probe.cu), so the box starts A >= R cells left of the tile.
+  static constexpr int AE = 16 / (int)sizeof(T);          // cells per 16 bytes
+  static constexpr int A = box_align_left(R, (int)sizeof(T));  // aligned left halo
+  static constexpr int BX = box_width(R, (int)sizeof(T));
   static constexpr int BY = TY + 2 * R;
+  static constexpr int OFF = 4 - R;                        // row-load phase
   static constexpr int STAGE_BYTES = BX * BY * (int)sizeof(T);
   static constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
-  static constexpr int SMEM = STAGES * STAGE_PITCH + 128;  // + barriers
+  static constexpr int SMEM = STAGES * STAGE_PITCH + 128 + 128;  // + barriers + align slack
+  static_assert(R >= 1 && R <= 4, "radius");
   static_assert(BX <= 256 && BY <= 256, "TMA box too large");
+  static_assert(4 * (TX / XPT - 1) + A - 4 + 4 * ((OFF + XPT + 2 * R + 3) / 4) <= BX, "row over-read");
 };
 
 template <int K>
@@ -133,16 +146,16 @@ __device__ __forceinline__ const T* plane_ptr(const TmaParams& p, PlaneSrc s) {
 }
 
 // ---------------------------------------------------------------------------
-// Row loads from shared memory: 4 + 2R consecutive cells starting at an
-// element offset that is a multiple of 4, widened to float.
+// Row loads from shared memory: N consecutive cells starting OFF cells after
+// a 4-cell-aligned address, widened to float.
 // ---------------------------------------------------------------------------
-template <typename T, int N>
+template <typename T, int N, int OFF>
 struct RowLoader;
 
-template <int N>
-struct RowLoader<float, N> {
+template <int N, int OFF>
+struct RowLoader<float, N, OFF> {
   __device__ __forceinline__ static void load(const float* row, float (&v)[N]) {
-    constexpr int NV = (N + 3) / 4;
+    constexpr int NV = (OFF + N + 3) / 4;
     float tmp[NV * 4];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -153,14 +166,14 @@ struct RowLoader<float, N> {
       tmp[4 * i + 3] = q.w;
     }
 #pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = tmp[i];
+    for (int i = 0; i < N; ++i) v[i] = tmp[OFF + i];
   }
 };
 
-template <int N>
-struct RowLoader<uint16_t, N> {
+template <int N, int OFF>
+struct RowLoader<uint16_t, N, OFF> {
   __device__ __forceinline__ static void load(const uint16_t* row, float (&v)[N]) {
-    constexpr int NV = (N + 3) / 4;  // 8-byte loads of 4 cells
+    constexpr int NV = (OFF + N + 3) / 4;  // 8-byte loads of 4 cells
     uint32_t tmp[NV * 2];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -170,25 +183,27 @@ struct RowLoader<uint16_t, N> {
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      uint32_t w = tmp[i >> 1];
+      const int c = OFF + i;
+      uint32_t w = tmp[c >> 1];
       // place the 16-bit cell in the low mantissa of 2^23
-      uint32_t bits = __byte_perm(w, 0x4B000000u, (i & 1) ? 0x7432 : 0x7410);
+      uint32_t bits = __byte_perm(w, 0x4B000000u, (c & 1) ? 0x7432 : 0x7410);
       v[i] = __int_as_float(bits) - 8388608.0f;
     }
   }
 };
 
-template <int N>
-struct RowLoader<uint8_t, N> {
+template <int N, int OFF>
+struct RowLoader<uint8_t, N, OFF> {
   __device__ __forceinline__ static void load(const uint8_t* row, float (&v)[N]) {
-    constexpr int NV = (N + 3) / 4;  // 4-byte loads of 4 cells
+    constexpr int NV = (OFF + N + 3) / 4;  // 4-byte loads of 4 cells
     uint32_t tmp[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) tmp[i] = reinterpret_cast<const uint32_t*>(row)[i];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      uint32_t w = tmp[i >> 2];
-      uint32_t sel = 0x7440u | (uint32_t)(i & 3);
+      const int c = OFF + i;
+      uint32_t w = tmp[c >> 2];
+      uint32_t sel = 0x7440u | (uint32_t)(c & 3);
       v[i] = __int_as_float(__byte_perm(w, 0x4B000000u, sel)) - 8388608.0f;
     }
   }
@@ -226,7 +241,7 @@ __device__ __forceinline__ void plane_step(const T* __restrict__ stage, int tx, 
 #pragma unroll
   for (int dy = 0; dy < K; ++dy) {
     float v[N];
-    RowLoader<T, N>::load(stage + (ty + dy) * G::BX + tx * XPT, v);
+    RowLoader<T, N, G::OFF>::load(stage + (ty + dy) * G::BX + tx * XPT + G::A - 4, v);
 #pragma unroll
     for (int m = 0; m < K; ++m) {
       if (GUARD && (m < first_slot || m > last_slot)) continue;
@@ -249,7 +264,9 @@ __global__ void __launch_bounds__(THREADS, 2)
                       const Weights<K> wt) {
   constexpr int R = K / 2;
   using G = Geo<T, R>;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // TMA destinations must be 128-byte aligned; do not rely on the base.
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_PITCH);
 
   const int tid = threadIdx.x;
@@ -280,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     const CUtensorMap* m = src.which == 0 ? &map_src : src.which == 1 ? &map_lo : &map_hi;
     mbar_arrive_tx(&bars[s], G::STAGE_BYTES);
-    tma_load_3d(dst, m, &bars[s], x0 - R, y0 - R, src.z);
+    tma_load_3d(dst, m, &bars[s], x0 - G::A, y0 - R, src.z);
   };
 
   if (tid == 0) {
@@ -314,9 +331,10 @@ __global__ void __launch_bounds__(THREADS, 2)
     } else if (MODE != VKT_BORDER && edge) {
       // out-of-range halo cells: gather the address-mapped cell
       const T* plane = plane_ptr<T>(p, src);
-      for (int q = tid; q < G::BY * G::W; q += THREADS) {
-        const int by = q / G::W, bx = q - by * G::W;
-        const int gx = x0 - R + bx, gy = y0 - R + by;
+      constexpr int W = TX + 2 * R;  // cells actually read: box x in [A-R, A+TX+R)
+      for (int q = tid; q < G::BY * W; q += THREADS) {
+        const int by = q / W, bx = q - by * W + (G::A - R);
+        const int gx = x0 - G::A + bx, gy = y0 - R + by;
         if (gx >= 0 && gx < p.nx && gy >= 0 && gy < p.ny) continue;
         const int mx = map_index32<MODE>(gx, p.nx);
         const int my = map_index32<MODE>(gy, p.ny);

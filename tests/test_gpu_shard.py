@@ -1,0 +1,150 @@
+"""GPU: z-slab sharded ApplyFilter emulated on one GPU.
+
+P "ranks" are P slabs of one volume on cuda:0; the halo exchange uses the
+same plan as the NCCL path with in-process copies (no kernel waits on another
+kernel).  Each slab runs the real interior / boundary launches with halos, and
+the concatenated result must be bit-identical to the unsharded ApplyFilter
+(the property the 8-GPU path relies on).  Large-volume tests check
+size-independent properties at BASELINE sizes.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2203_10213_b200 as vk
+from paper_2203_10213_b200.shard import ShardedVolume, apply_filter_sharded, plan_halos
+
+pytestmark = pytest.mark.gpu
+
+
+def _sharded_run(host, fmt, kernel, mode, world, path="auto"):
+    import torch
+
+    nz, ny, nx = host.shape
+    srcs, dsts = [], []
+    for r in range(world):
+        s = ShardedVolume((nx, ny, nz), fmt, r, world)
+        s.local.upload(np.ascontiguousarray(host[s.z0:s.z1]))
+        srcs.append(s)
+        dsts.append(ShardedVolume((nx, ny, nz), fmt, r, world))
+
+    def local_exchange(plan, rank, planes, lo, hi):
+        # same semantics as exchange_halos, peers' planes read in-process
+        halos = {"lo": lo, "hi": hi}
+        for t in plan.transfers:
+            if t.dst_rank == rank:
+                halos[t.side][t.dst_first:t.dst_first + t.count].copy_(
+                    srcs[t.src_rank].planes()[t.src_first:t.src_first + t.count])
+        for (r, side, slot) in plan.border:
+            if r == rank:
+                halos[side][slot].zero_()
+
+    vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
+    try:
+        for r in range(world):
+            apply_filter_sharded(dsts[r], srcs[r], kernel, mode, exchange=local_exchange)
+    finally:
+        vk.set_execution_policy(vk.ExecutionPolicy())
+    torch.cuda.synchronize()
+    return np.concatenate([d.local.to_numpy() for d in dsts])
+
+
+def _unsharded(host, fmt, kernel, mode, path="auto"):
+    src = vk.StructuredVolume.from_numpy(host, fmt)
+    dst = vk.StructuredVolume(src.dims, fmt)
+    vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
+    try:
+        vk.ApplyFilter(dst, src, kernel, mode)
+    finally:
+        vk.set_execution_policy(vk.ExecutionPolicy())
+    return dst.to_numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("mode", list(vk.AddressMode))
+@pytest.mark.parametrize("fmt,k", [(vk.DataFormat.UINT16, 7), (vk.DataFormat.FLOAT32, 3),
+                                   (vk.DataFormat.UINT8, 5)])
+def test_sharded_bit_identical_to_unsharded(world, mode, fmt, k):
+    rng = np.random.default_rng(world * 100 + k)
+    shape = (40, 24, 64)  # (z, y, x): TMA-eligible rows for every format
+    host = (rng.random(shape, dtype=np.float32) if fmt is vk.DataFormat.FLOAT32 else
+            rng.integers(0, np.iinfo(fmt.dtype).max + 1, size=shape, dtype=fmt.dtype))
+    kern = vk.gaussian_kernel(1.0, k) if k != 5 else vk.box_kernel(5)
+    want = _unsharded(host, fmt, kern, mode)
+    got = _sharded_run(host, fmt, kern, mode, world)
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+@pytest.mark.parametrize("path", ["direct", "exact"])
+def test_sharded_other_paths(path):
+    rng = np.random.default_rng(4)
+    host = rng.integers(0, 65536, size=(11, 9, 13), dtype=np.uint16)
+    kern = vk.gaussian_kernel(1.5)  # rz=3 > slab thickness at world 4
+    for mode in vk.AddressMode:
+        want = _unsharded(host, vk.DataFormat.UINT16, kern, mode, path)
+        got = _sharded_run(host, vk.DataFormat.UINT16, kern, mode, 4, path)
+        assert np.array_equal(got, want), mode
+
+
+def test_plan_matches_bench_layout():
+    plan = plan_halos(1024, 8, 3, "clamp")
+    assert sum(t.count for t in plan.transfers) == 8 * 2 * 3
+
+
+# ---- full-size, size-independent properties (BASELINE configs) ----
+
+def test_cfg3_1024_u16_delta_is_identity_and_constant_is_fixed():
+    import torch
+
+    dims = (1024, 1024, 1024)
+    src = vk.synthetic_device(dims, vk.DataFormat.UINT16, seed=3)
+    dst = vk.StructuredVolume(src.dims, src.format, data=vk.DeviceBuffer(src.nbytes, zero=False))
+    w = np.zeros((7, 7, 7))
+    w[3, 3, 3] = 1.0
+    vk.ApplyFilter(dst, src, vk.Kernel((7, 7, 7), w))
+    assert torch.equal(dst.data.array, src.data.array)
+    vk.fill(src, 0.5)
+    vk.ApplyFilter(dst, src, vk.gaussian_kernel(1.5))
+    # torch has no uint16 reductions: compare the raw 16-bit pattern (32768 = 0x8000)
+    assert bool((dst.array().view(torch.int16) == -32768).all())
+    del src, dst
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_wrap_laplacian_sums_to_zero_f32():
+    """Wrap mode is periodic: sum(out) = sum(w) * sum(in) = 0 for the Laplacian."""
+    import torch
+
+    dims = (512, 512, 512)
+    src = vk.synthetic_device(dims, vk.DataFormat.FLOAT32, seed=9)
+    dst = vk.StructuredVolume(src.dims, src.format)
+    vk.ApplyFilter(dst, src, vk.laplacian_kernel(), vk.AddressMode.WRAP)
+    total = dst.array().double().sum().item()
+    scale = src.array().double().abs().sum().item()
+    assert abs(total) <= 1e-6 * scale
+    # and box5 in Wrap mode preserves the total
+    vk.ApplyFilter(dst, src, vk.box_kernel(5), vk.AddressMode.WRAP)
+    s_in = src.array().double().sum().item()
+    s_out = dst.array().double().sum().item()
+    assert abs(s_out - s_in) <= 1e-5 * abs(s_in)
+    del src, dst
+    torch.cuda.empty_cache()
+
+
+def test_cfg2_512_f32_box5_mirror_chunk_vs_oracle():
+    """Full 512^3 on the GPU; a z-chunk of it against the oracle (chunked runner)."""
+    import torch
+    from oracle import vkt_oracle as O
+
+    dims = (512, 512, 512)
+    src = vk.synthetic_device(dims, vk.DataFormat.FLOAT32, seed=21)
+    dst = vk.StructuredVolume(src.dims, src.format)
+    vk.ApplyFilter(dst, src, vk.box_kernel(5), vk.AddressMode.MIRROR)
+    host = src.to_numpy()
+    for z0, z1 in ((0, 3), (254, 258), (509, 512)):
+        want = O.apply_filter(host, 3, O.box_weights(5), "mirror", z_range=(z0, z1))
+        got = dst.array()[z0:z1].cpu().numpy()
+        d = np.abs(got.astype(np.float64) - want)
+        assert np.all(d <= 1e-5 * np.abs(want) + 1e-5)
+    del src, dst
+    torch.cuda.empty_cache()

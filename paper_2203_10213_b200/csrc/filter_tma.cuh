@@ -1,28 +1,32 @@
-// filter_tma.cuh — tiled sm_100a ApplyFilter kernel.
+// filter_tma.cuh — tiled, warp-specialised sm_100a ApplyFilter kernel.
 //
 // Design:
-//  * A CTA owns a 64 (x) by 16 (y) column of outputs and a chunk of ZC output
-//    planes.  It streams the input planes of that chunk through a ring of S
-//    shared-memory stages; each stage is ONE TMA 3D box load
-//    (cp.async.bulk.tensor.3d) of the plane's (64+2R) x (16+2R) footprint,
-//    completed on an mbarrier (complete_tx).  One elected thread issues the
-//    TMA for plane i+S-1 while all 256 threads compute plane i.
-//  * Each thread owns 4 consecutive x outputs of one row and keeps K = 2R+1
-//    rolling register accumulators per output, one per output plane the
-//    current input plane contributes to (the "register-blocked run of
-//    outputs along z").  Per input plane and row dy it loads the 4+2R inputs
-//    once (128/64/32-bit LDS) and issues 4*K*K FFMAs with the weight as a
-//    constant-bank operand (the weights are a by-value kernel parameter).
+//  * A CTA owns a TX=128 (x) by TY=16 (y) column of outputs and a chunk of ZC
+//    output planes, and streams the chunk's input planes through shared
+//    memory.  Each input plane is ONE TMA 3D box load
+//    (cp.async.bulk.tensor.3d, completion on an mbarrier with complete_tx) of
+//    the plane's footprint plus its halo.
+//  * No dedicated producer warp (it would leave its SM sub-partition with
+//    fewer FMA warps than the other three, measured: 85% issue).  All 8 warps
+//    compute, and each also does 1/8 of the staging of the NEXT plane:
+//    repairing the out-of-volume halo cells of edge tiles for Clamp / Mirror
+//    / Wrap (Border is TMA's zero fill = stored 0) and, for u8/u16 volumes,
+//    widening the raw TMA plane to float once per cell into a "ready" stage.
+//    Lane 0 of warp 0 issues the TMA loads.  Warps meet only on mbarriers
+//    (full / ready / empty rings); there is no CTA-wide barrier per plane.
+//  * Compute warps: each thread owns 8 consecutive x outputs of one row and
+//    keeps K = 2R+1 rolling register accumulators per output — one per output
+//    plane the current input plane contributes to (the register-blocked run of
+//    outputs along z).  Per input plane the dy loop stays rolled (the body is
+//    ~K*K*8 FFMAs, small enough for the instruction cache); each dy iteration
+//    loads 16 floats of the input row (4 x LDS.128) and issues 8*K*K FFMAs
+//    whose weight operand is a uniform register (LDCU from the by-value
+//    kernel-parameter block, rows padded to 16 bytes).
 //  * Tap order per output is (dz, dy, dx) — the reference's order
-//    (filters.py:89-92) and the direct kernel's — so every path and every
-//    z-slab split produce bit-identical results.
-//  * Boundary handling: Border = TMA's out-of-bounds zero fill (stored 0);
-//    Clamp/Mirror/Wrap tiles on the volume edge overwrite their out-of-range
-//    halo cells after the TMA lands ("fixup"), compile-time specialised per
-//    mode; z is resolved per plane (local slab, halo buffer, or mapped plane).
-//  * Integer voxels are widened with the exponent trick (ALU+FMA pipes) and
-//    the epilogue quantizes as volume.py:102-110; outputs are stored with
-//    streaming (evict-first) vector stores.
+//    (filters.py:89-92) and the direct kernel's — so every kernel path and
+//    every z-slab split produce bit-identical results.
+//  * Epilogue: quantize as volume.py:102-110 (ints) and store with streaming
+//    (evict-first) 128-bit stores.
 #pragma once
 
 #include <cuda.h>
@@ -32,13 +36,16 @@
 namespace vkt {
 namespace tma {
 
-constexpr int TX = 64;     // outputs per CTA in x
-constexpr int TY = 16;     // outputs per CTA in y
-constexpr int XPT = 4;     // outputs per thread in x
-constexpr int THREADS = (TX / XPT) * TY;  // 256
-constexpr int STAGES = 4;
+constexpr int TX = 128;          // outputs per CTA in x
+constexpr int XPT = 8;           // outputs per compute thread in x
+constexpr int WARPS = 8;         // 2 CTAs/SM -> 4 warps per SMSP -> 128 registers
+constexpr int TY = WARPS * 32 / (TX / XPT);  // 16 output rows per CTA
+constexpr int THREADS = 32 * WARPS;
+constexpr int RP = TX + 8;       // ready-stage row pitch (floats): x in [x0-4, x0+TX+4)
 
-// Box geometry shared by the host (tensor-map encode) and the kernel.
+// Raw TMA box geometry (shared by the host tensor-map encode and the kernel).
+// TMA needs the innermost box coordinate at a 16-byte multiple (measured with
+// tools/tma_probe.cu), so the box starts A >= R cells left of the tile.
 __host__ __device__ constexpr int box_align_left(int r, int bpc) {
   return (r + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
 }
@@ -46,26 +53,36 @@ __host__ __device__ constexpr int box_width(int r, int bpc) {
   return (box_align_left(r, bpc) + TX + r + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
 }
 
-template <typename T, int R>
-struct Geo {
-  // TMA needs the innermost box coordinate at a 16-byte multiple (measured:
-  // tools/tma_probe.cu), so the box starts A >= R cells left of the tile.
-  static constexpr int AE = 16 / (int)sizeof(T);          // cells per 16 bytes
-  static constexpr int A = box_align_left(R, (int)sizeof(T));  // aligned left halo
+template <typename T, int K>
+struct Cfg {
+  static constexpr int R = K / 2;
+  static constexpr bool IS_F32 = sizeof(T) == 4;
+  static constexpr int A = box_align_left(R, (int)sizeof(T));
   static constexpr int BX = box_width(R, (int)sizeof(T));
   static constexpr int BY = TY + 2 * R;
-  static constexpr int OFF = 4 - R;                        // row-load phase
-  static constexpr int STAGE_BYTES = BX * BY * (int)sizeof(T);
-  static constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
-  static constexpr int SMEM = STAGES * STAGE_PITCH + 128 + 128;  // + barriers + align slack
+  static constexpr int RAW_BYTES = BX * BY * (int)sizeof(T);
+  static constexpr int RAW_PITCH = (RAW_BYTES + 127) / 128 * 128;
+  static constexpr int RDY_BYTES = RP * BY * 4;
+  static constexpr int RDY_PITCH = (RDY_BYTES + 127) / 128 * 128;
+  // ready-ring depth (f32: TMA lands here directly, so it is also the TMA
+  // lookahead; small K needs more planes in flight to cover HBM latency)
+  static constexpr int S_RDY = IS_F32 ? (K == 3 ? 10 : K == 5 ? 6 : 5) : 4;
+  static constexpr int S_RAW = IS_F32 ? 0 : (K == 3 ? 10 : K == 5 ? 6 : 5);
+  static constexpr int AHEAD = 2;  // ints: planes converted ahead of compute
+  static constexpr int SMEM_DATA = S_RDY * RDY_PITCH + S_RAW * RAW_PITCH;
+  static constexpr int NBAR = 2 * S_RDY + 2 * (IS_F32 ? S_RDY : S_RAW);
+  static constexpr int SMEM = SMEM_DATA + NBAR * 8 + 128;
+  static_assert(!IS_F32 || BX == RP, "f32 TMA box must match the ready layout");
   static_assert(R >= 1 && R <= 4, "radius");
   static_assert(BX <= 256 && BY <= 256, "TMA box too large");
-  static_assert(4 * (TX / XPT - 1) + A - 4 + 4 * ((OFF + XPT + 2 * R + 3) / 4) <= BX, "row over-read");
 };
 
+// Weights as a kernel-parameter block, each (dz, dy) row of K taps padded to a
+// 16-byte boundary so a row is fetched with 128-bit uniform constant loads.
 template <int K>
-struct Weights {
-  float w[K * K * K];
+struct alignas(16) Weights {
+  static constexpr int KP = (K + 3) / 4 * 4;
+  float w[K * K * KP];
 };
 
 struct TmaParams {
@@ -114,6 +131,29 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+// Predicated single-thread forms: executed by every thread of the CTA with
+// the predicate true in exactly one, so the surrounding loop stays free of
+// thread-divergent branches (ptxas then keeps the rolled dy loop's weight
+// loads on the uniform datapath: LDCU + FFMA with a uniform-register operand).
+__device__ __forceinline__ void mbar_arrive_if(uint64_t* bar, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tsetp.ne.b32 P, %1, 0;\n\t"
+      "@P mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(smem_u32(bar)),
+      "r"((int)pred)
+      : "memory");
+}
+__device__ __forceinline__ void tma_issue_if(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                             uint32_t bytes, int x, int y, int z, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tsetp.ne.b32 P, %7, 0;\n\t"
+      "@P fence.proxy.async.shared::cta;\n\t"
+      "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%5], %6;\n\t"
+      "@P cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "r"(bytes),
+      "r"((int)pred)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -121,11 +161,11 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// Plane source for local extended plane e: which map + coordinate, or a zero
-// (Border) plane.  Also returns the global pointer for fixup gathers.
+// Plane source for local extended plane e (0 local, 1 halo_lo, 2 halo_hi,
+// -1 Border zero plane) and its index within that tensor.
 struct PlaneSrc {
-  int which;  // 0 local, 1 halo_lo, 2 halo_hi, -1 zero plane
-  int z;      // plane index within that tensor
+  int which;
+  int z;
 };
 
 template <int MODE>
@@ -145,112 +185,202 @@ __device__ __forceinline__ const T* plane_ptr(const TmaParams& p, PlaneSrc s) {
   return static_cast<const T*>(base) + (int64_t)s.z * pe;
 }
 
+__device__ __forceinline__ float widen(float v) { return v; }
+__device__ __forceinline__ float widen(uint16_t v) { return to_f32(v); }
+__device__ __forceinline__ float widen(uint8_t v) { return to_f32(v); }
+
+// Value of the (address-mapped) cell (gx, gy) of a plane; Border never calls.
+template <typename T, int MODE>
+__device__ __forceinline__ float gather_cell(const T* plane, const TmaParams& p, int gx, int gy) {
+  const int mx = map_index32<MODE>(gx, p.nx);
+  const int my = map_index32<MODE>(gy, p.ny);
+  return widen(__ldg(plane + (int64_t)my * p.nx + mx));
+}
+
 // ---------------------------------------------------------------------------
-// Row loads from shared memory: N consecutive cells starting OFF cells after
-// a 4-cell-aligned address, widened to float.
+// Producer helpers
 // ---------------------------------------------------------------------------
-template <typename T, int N, int OFF>
-struct RowLoader;
-
-template <int N, int OFF>
-struct RowLoader<float, N, OFF> {
-  __device__ __forceinline__ static void load(const float* row, float (&v)[N]) {
-    constexpr int NV = (OFF + N + 3) / 4;
-    float tmp[NV * 4];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      float4 q = reinterpret_cast<const float4*>(row)[i];
-      tmp[4 * i + 0] = q.x;
-      tmp[4 * i + 1] = q.y;
-      tmp[4 * i + 2] = q.z;
-      tmp[4 * i + 3] = q.w;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = tmp[OFF + i];
+// Out-of-volume cells of the ready (f32) stage that outputs of this tile
+// read: x in [x0-R, min(x0+TX,nx)+R), y in [y0-R, min(y0+TY,ny)+R), excluding
+// in-volume cells.  Enumerated as full rows above/below the volume plus
+// left/right strips.
+struct EdgeCells {
+  int xa, ya, w, top, nl, side, n_rows, total;
+  __device__ __forceinline__ EdgeCells(const TmaParams& p, int x0, int y0, int R, int row_lo,
+                                       int row_hi) {
+    xa = x0 - R;
+    const int xb = min(x0 + TX, p.nx) + R;
+    ya = max(y0 - R, y0 - R + row_lo);
+    const int yb = min(min(y0 + TY, p.ny) + R, y0 - R + row_hi);
+    w = xb - xa;
+    const int rows = max(0, yb - ya);
+    top = min(rows, max(0, -ya));
+    const int bot = min(rows - top, max(0, yb - p.ny));
+    nl = max(0, -xa);
+    side = nl + max(0, xb - p.nx);
+    n_rows = (top + bot) * w;
+    total = n_rows + (rows - top - bot) * side;
   }
-};
-
-template <int N, int OFF>
-struct RowLoader<uint16_t, N, OFF> {
-  __device__ __forceinline__ static void load(const uint16_t* row, float (&v)[N]) {
-    constexpr int NV = (OFF + N + 3) / 4;  // 8-byte loads of 4 cells
-    uint32_t tmp[NV * 2];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      uint2 q = reinterpret_cast<const uint2*>(row)[i];
-      tmp[2 * i + 0] = q.x;
-      tmp[2 * i + 1] = q.y;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const int c = OFF + i;
-      uint32_t w = tmp[c >> 1];
-      // place the 16-bit cell in the low mantissa of 2^23
-      uint32_t bits = __byte_perm(w, 0x4B000000u, (c & 1) ? 0x7432 : 0x7410);
-      v[i] = __int_as_float(bits) - 8388608.0f;
+  __device__ __forceinline__ void cell(const TmaParams& p, int q, int& gx, int& gy) const {
+    if (q < n_rows) {
+      const int r = q / w;
+      gy = r < top ? ya + r : p.ny + (r - top);
+      gx = xa + (q - r * w);
+    } else {
+      const int q2 = q - n_rows;
+      const int r = q2 / side;
+      const int c = q2 - r * side;
+      gy = ya + top + r;
+      gx = c < nl ? xa + c : p.nx + (c - nl);
     }
   }
 };
 
-template <int N, int OFF>
-struct RowLoader<uint8_t, N, OFF> {
-  __device__ __forceinline__ static void load(const uint8_t* row, float (&v)[N]) {
-    constexpr int NV = (OFF + N + 3) / 4;  // 4-byte loads of 4 cells
-    uint32_t tmp[NV];
+// f32 stages: repair this thread's share (t of nt) of the edge cells.  Clamp
+// and Mirror map every such cell onto an in-volume cell inside the staged box
+// (R <= 4 < TX, TY), so those are shared-memory copies from cells the TMA
+// delivered; Wrap maps to the opposite face and gathers from global memory
+// (8 loads in flight per thread).  Border never calls (TMA zero fill).
+template <int MODE, int R>
+__device__ __forceinline__ void fixup_f32(float* stage, const float* plane, const TmaParams& p,
+                                          int x0, int y0, int t, int nt, int row_lo, int row_hi) {
+  // only rows [row_lo, row_hi) of the stage (a warp's read window)
+  const EdgeCells ec(p, x0, y0, R, row_lo, row_hi);
+  constexpr int B = 8;
+  for (int base = t; base < ec.total; base += nt * B) {
+    float val[B];
+    int dst[B];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) tmp[i] = reinterpret_cast<const uint32_t*>(row)[i];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const int c = OFF + i;
-      uint32_t w = tmp[c >> 2];
-      uint32_t sel = 0x7440u | (uint32_t)(c & 3);
-      v[i] = __int_as_float(__byte_perm(w, 0x4B000000u, sel)) - 8388608.0f;
+    for (int b = 0; b < B; ++b) {
+      const int q = base + b * nt;
+      dst[b] = -1;
+      if (q < ec.total) {
+        int gx, gy;
+        ec.cell(p, q, gx, gy);
+        const int mx = map_index32<MODE>(gx, p.nx);
+        const int my = map_index32<MODE>(gy, p.ny);
+        dst[b] = (gy - y0 + R) * RP + (gx - x0 + 4);
+        if constexpr (MODE == VKT_WRAP)
+          val[b] = __ldg(plane + (int64_t)my * p.nx + mx);
+        else
+          val[b] = stage[(my - y0 + R) * RP + (mx - x0 + 4)];
+      }
     }
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (dst[b] >= 0) stage[dst[b]] = val[b];
   }
-};
+}
 
+// u8/u16: widen this thread's share of the raw TMA plane into the ready stage
+// (layout: x from x0-4).  On edge tiles the out-of-volume cells are replaced
+// by their address-mapped value, read from the raw stage (Clamp / Mirror) or
+// gathered from global memory (Wrap); Border keeps the TMA zero fill.
+template <typename T, int MODE, int K>
+__device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T* plane,
+                                              const TmaParams& p, int x0, int y0, bool edge, int t,
+                                              int nt) {
+  using C = Cfg<T, K>;
+  constexpr int R = C::R;
+  constexpr int QPR = RP / 4;  // quads per row
+  constexpr int NQ = QPR * C::BY;
+#pragma unroll 2
+  for (int q = t; q < NQ; q += nt) {
+    const int by = q / QPR;
+    const int e = (q - by * QPR) * 4;  // ready index of the quad's first cell
+    const T* src = raw + by * C::BX + e + (C::A - 4);
+    float f[4];
+    if constexpr (sizeof(T) == 2) {
+      const uint2 w = *reinterpret_cast<const uint2*>(src);
+      f[0] = __int_as_float(__byte_perm(w.x, 0x4B000000u, 0x7410)) - 8388608.0f;
+      f[1] = __int_as_float(__byte_perm(w.x, 0x4B000000u, 0x7432)) - 8388608.0f;
+      f[2] = __int_as_float(__byte_perm(w.y, 0x4B000000u, 0x7410)) - 8388608.0f;
+      f[3] = __int_as_float(__byte_perm(w.y, 0x4B000000u, 0x7432)) - 8388608.0f;
+    } else {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(src);
+      f[0] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7440)) - 8388608.0f;
+      f[1] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7441)) - 8388608.0f;
+      f[2] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7442)) - 8388608.0f;
+      f[3] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7443)) - 8388608.0f;
+    }
+    if (MODE != VKT_BORDER && edge) {
+      const int gy = y0 - R + by;
+      const bool yo = gy < 0 || gy >= p.ny;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int gx = x0 - 4 + e + c;
+        if ((yo || gx < 0 || gx >= p.nx) && gx >= x0 - R && gx < x0 + TX + R) {
+          const int mx = map_index32<MODE>(gx, p.nx);
+          const int my = map_index32<MODE>(gy, p.ny);
+          if constexpr (MODE == VKT_WRAP)
+            f[c] = widen(__ldg(plane + (int64_t)my * p.nx + mx));
+          else
+            f[c] = widen(raw[(my - y0 + R) * C::BX + (mx - x0 + C::A)]);
+        }
+      }
+    }
+    *reinterpret_cast<float4*>(rdy + by * RP + e) = make_float4(f[0], f[1], f[2], f[3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Compute helpers
+// ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void store4(T* out, const float (&acc)[XPT], float c);
+__device__ __forceinline__ void store8(T* out, const float (&a)[XPT], float c, int valid);
 
 template <>
-__device__ __forceinline__ void store4<float>(float* out, const float (&a)[XPT], float) {
-  __stcs(reinterpret_cast<float4*>(out), make_float4(a[0], a[1], a[2], a[3]));
+__device__ __forceinline__ void store8<float>(float* out, const float (&a)[XPT], float, int valid) {
+  if (valid >= 4) __stcs(reinterpret_cast<float4*>(out), make_float4(a[0], a[1], a[2], a[3]));
+  if (valid >= 8) __stcs(reinterpret_cast<float4*>(out) + 1, make_float4(a[4], a[5], a[6], a[7]));
 }
 template <>
-__device__ __forceinline__ void store4<uint16_t>(uint16_t* out, const float (&a)[XPT], float c) {
-  uint32_t q0 = quantize_f32<uint16_t>(a[0], c), q1 = quantize_f32<uint16_t>(a[1], c);
-  uint32_t q2 = quantize_f32<uint16_t>(a[2], c), q3 = quantize_f32<uint16_t>(a[3], c);
-  __stcs(reinterpret_cast<uint2*>(out), make_uint2(q0 | (q1 << 16), q2 | (q3 << 16)));
-}
-template <>
-__device__ __forceinline__ void store4<uint8_t>(uint8_t* out, const float (&a)[XPT], float c) {
-  uint32_t q0 = quantize_f32<uint8_t>(a[0], c), q1 = quantize_f32<uint8_t>(a[1], c);
-  uint32_t q2 = quantize_f32<uint8_t>(a[2], c), q3 = quantize_f32<uint8_t>(a[3], c);
-  __stcs(reinterpret_cast<unsigned int*>(out), q0 | (q1 << 8) | (q2 << 16) | (q3 << 24));
-}
-
-// One input plane's contribution to the K rolling accumulators.
-// GUARD: skip slots whose output plane is outside the chunk (ramp up/down).
-template <typename T, int K, bool GUARD>
-__device__ __forceinline__ void plane_step(const T* __restrict__ stage, int tx, int ty,
-                                           const Weights<K>& wt, float (&acc)[K][XPT], int first_slot,
-                                           int last_slot) {
-  constexpr int R = K / 2;
-  constexpr int N = XPT + 2 * R;
-  using G = Geo<T, R>;
+__device__ __forceinline__ void store8<uint16_t>(uint16_t* out, const float (&a)[XPT], float c, int) {
+  uint32_t q[XPT];
 #pragma unroll
+  for (int j = 0; j < XPT; ++j) q[j] = quantize_f32<uint16_t>(a[j], c);
+  __stcs(reinterpret_cast<uint4*>(out),
+         make_uint4(q[0] | (q[1] << 16), q[2] | (q[3] << 16), q[4] | (q[5] << 16), q[6] | (q[7] << 16)));
+}
+template <>
+__device__ __forceinline__ void store8<uint8_t>(uint8_t* out, const float (&a)[XPT], float c, int) {
+  uint32_t q[XPT];
+#pragma unroll
+  for (int j = 0; j < XPT; ++j) q[j] = quantize_f32<uint8_t>(a[j], c);
+  __stcs(reinterpret_cast<uint2*>(out), make_uint2(q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24),
+                                                   q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24)));
+}
+
+// One input plane's contribution to the K rolling accumulators of 8 outputs.
+// GUARD: skip slots whose output plane is outside the chunk (ramp up/down).
+template <int K, bool GUARD>
+__device__ __forceinline__ void plane_step(const float* __restrict__ stage, int tx, int ty,
+                                           const Weights<K>& wt, float (&acc)[K][XPT], int first,
+                                           int last) {
+  constexpr int R = K / 2;
+  constexpr int OFF = 4 - R;
+#pragma unroll(K <= 3 ? K : 1)
   for (int dy = 0; dy < K; ++dy) {
-    float v[N];
-    RowLoader<T, N, G::OFF>::load(stage + (ty + dy) * G::BX + tx * XPT + G::A - 4, v);
+    const float4* row = reinterpret_cast<const float4*>(stage + (ty + dy) * RP + XPT * tx);
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 q = row[i];
+      v[4 * i + 0] = q.x;
+      v[4 * i + 1] = q.y;
+      v[4 * i + 2] = q.z;
+      v[4 * i + 3] = q.w;
+    }
 #pragma unroll
     for (int m = 0; m < K; ++m) {
-      if (GUARD && (m < first_slot || m > last_slot)) continue;
+      if (GUARD && (m < first || m > last)) continue;
       const int dz = K - 1 - m;
+      const float* w = wt.w + (dz * K + dy) * Weights<K>::KP;
 #pragma unroll
       for (int dx = 0; dx < K; ++dx) {
-        const float w = wt.w[(dz * K + dy) * K + dx];
+        const float wv = w[dx];
 #pragma unroll
-        for (int j = 0; j < XPT; ++j) acc[m][j] = __fmaf_rn(w, v[j + dx], acc[m][j]);
+        for (int j = 0; j < XPT; ++j) acc[m][j] = __fmaf_rn(wv, v[OFF + j + dx], acc[m][j]);
       }
     }
   }
@@ -261,17 +391,25 @@ __global__ void __launch_bounds__(THREADS, 2)
     filter_tma_kernel(const __grid_constant__ CUtensorMap map_src,
                       const __grid_constant__ CUtensorMap map_lo,
                       const __grid_constant__ CUtensorMap map_hi, const TmaParams p,
-                      const Weights<K> wt) {
-  constexpr int R = K / 2;
-  using G = Geo<T, R>;
+                      const __grid_constant__ Weights<K> wt) {
+  using C = Cfg<T, K>;
+  constexpr int R = C::R;
+  constexpr int S = C::S_RDY;
+  constexpr int SR = C::IS_F32 ? C::S_RDY : C::S_RAW;  // TMA ring depth
   extern __shared__ __align__(128) uint8_t smem_raw[];
   // TMA destinations must be 128-byte aligned; do not rely on the base.
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_PITCH);
+  float* rdy_base = reinterpret_cast<float*>(smem);
+  T* raw_base = reinterpret_cast<T*>(smem + C::S_RDY * C::RDY_PITCH);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA);
+  uint64_t* full = bars;            // [SR] TMA landed (f32: in the ready ring)
+  uint64_t* ready = full + SR;      // [S]  staged plane complete (8 warp arrivals)
+  uint64_t* empty = ready + S;      // [S]  all warps done computing from the stage
+  uint64_t* raw_free = empty + S;   // [SR] ints: all warps done converting the raw stage
 
   const int tid = threadIdx.x;
-  const int tx = tid % (TX / XPT);
-  const int ty = tid / (TX / XPT);
+  const int warp = tid / 32;
+  const int lane = tid % 32;
   const int x0 = blockIdx.x * TX;
   const int y0 = blockIdx.y * TY;
   const int zo0 = p.z_begin + blockIdx.z * p.zc;
@@ -282,28 +420,64 @@ __global__ void __launch_bounds__(THREADS, 2)
 
   if (tid == 0) {
     prefetch_tmap(&map_src);
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < SR; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&raw_free[s], WARPS);
+    }
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&ready[s], WARPS);
+      mbar_init(&empty[s], WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  auto produce = [&](int i) {
-    const int s = i % STAGES;
-    const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + i);
-    T* dst = reinterpret_cast<T*>(smem + s * G::STAGE_PITCH);
-    if (src.which < 0) {
-      mbar_arrive(&bars[s]);  // zero plane: consumers clear the stage
+  // TMA plane j into ring slot j % SR (zero planes: plain arrive).  Called
+  // by all threads; only thread 0 acts (predicated, no divergent branch).
+  const bool leader = tid == 0;
+  auto issue = [&](int j) {
+    const int r = j % SR;
+    void* dst = C::IS_F32 ? static_cast<void*>(rdy_base + r * (C::RDY_PITCH / 4))
+                          : static_cast<void*>(raw_base + r * (C::RAW_PITCH / (int)sizeof(T)));
+    const PlaneSrc s = resolve<MODE>(p, R, zo0 - R + j);
+    if (s.which < 0) {
+      mbar_arrive_if(&full[r], leader);
       return;
     }
-    const CUtensorMap* m = src.which == 0 ? &map_src : src.which == 1 ? &map_lo : &map_hi;
-    mbar_arrive_tx(&bars[s], G::STAGE_BYTES);
-    tma_load_3d(dst, m, &bars[s], x0 - G::A, y0 - R, src.z);
+    const CUtensorMap* m = s.which == 0 ? &map_src : s.which == 1 ? &map_lo : &map_hi;
+    tma_issue_if(dst, m, &full[r], C::IS_F32 ? C::RDY_BYTES : C::RAW_BYTES, x0 - C::A, y0 - R,
+                 s.z, leader);
   };
 
-  if (tid == 0) {
-    for (int i = 0; i < STAGES - 1 && i < np; ++i) produce(i);
+  // ints: widen plane j (all warps, 1/8 share each) into ready stage j % S.
+  auto prepare = [&](int j) {
+    const int s = j % S;
+    float* stage = rdy_base + s * (C::RDY_PITCH / 4);
+    const int r = j % SR;
+    mbar_wait(&full[r], (uint32_t)((j / SR) & 1));
+    if (j >= S) mbar_wait(&empty[s], (uint32_t)(((j / S) - 1) & 1));
+    const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + j);
+    if (src.which < 0) {
+      float4* w4 = reinterpret_cast<float4*>(stage);
+      for (int q = tid; q < C::RDY_BYTES / 16; q += THREADS) w4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const T* raw = raw_base + r * (C::RAW_PITCH / (int)sizeof(T));
+      convert_plane<T, MODE, K>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, edge, tid, THREADS);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&ready[s]);
+      mbar_arrive(&raw_free[r]);
+    }
+  };
+
+  for (int j = 0; j < SR && j < np; ++j) issue(j);
+  if constexpr (!C::IS_F32) {
+    for (int j = 0; j < C::AHEAD && j < np; ++j) prepare(j);
   }
 
+  const int tx = tid % (TX / XPT);
+  const int ty = tid / (TX / XPT);
   float acc[K][XPT];
 #pragma unroll
   for (int m = 0; m < K; ++m)
@@ -312,48 +486,59 @@ __global__ void __launch_bounds__(THREADS, 2)
 
   const int ox = x0 + tx * XPT;
   const int oy = y0 + ty;
-  const bool out_ok = (ox < p.nx) && (oy < p.ny);
+  const int valid = (oy < p.ny) ? min(XPT, p.nx - ox) : 0;
   T* out_base = static_cast<T*>(p.dst) + (int64_t)oy * p.nx + ox;
   const int64_t plane_elems = (int64_t)p.nx * p.ny;
 
   for (int i = 0; i < np; ++i) {
-    if (tid == 0 && i + STAGES - 1 < np) produce(i + STAGES - 1);
-    const int s = i % STAGES;
-    T* stage = reinterpret_cast<T*>(smem + s * G::STAGE_PITCH);
-    mbar_wait(&bars[s], (uint32_t)((i / STAGES) & 1));
-
-    const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + i);
-    if (src.which < 0) {
-      // Border zero plane (stored 0)
-      uint32_t* w = reinterpret_cast<uint32_t*>(stage);
-      for (int q = tid; q < G::STAGE_BYTES / 4; q += THREADS) w[q] = 0u;
-      __syncthreads();
-    } else if (MODE != VKT_BORDER && edge) {
-      // out-of-range halo cells: gather the address-mapped cell
-      const T* plane = plane_ptr<T>(p, src);
-      constexpr int W = TX + 2 * R;  // cells actually read: box x in [A-R, A+TX+R)
-      for (int q = tid; q < G::BY * W; q += THREADS) {
-        const int by = q / W, bx = q - by * W + (G::A - R);
-        const int gx = x0 - G::A + bx, gy = y0 - R + by;
-        if (gx >= 0 && gx < p.nx && gy >= 0 && gy < p.ny) continue;
-        const int mx = map_index32<MODE>(gx, p.nx);
-        const int my = map_index32<MODE>(gy, p.ny);
-        stage[by * G::BX + bx] = __ldg(plane + (int64_t)my * p.nx + mx);
+    const int s = i % S;
+    float* stage = rdy_base + s * (C::RDY_PITCH / 4);
+    if constexpr (C::IS_F32) {
+      // refill the TMA slot of plane i-2 (released by every warp by now, so
+      // warp 0 rarely waits)
+      if (i >= 2 && i + SR - 2 < np) {
+        mbar_wait(&empty[(i - 2) % S], (uint32_t)(((i - 2) / S) & 1));
+        issue(i + SR - 2);
       }
-      __syncthreads();
+      mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+      if (MODE != VKT_BORDER || edge) {
+        const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + i);
+        if (src.which < 0) {
+          // Border zero plane: this warp clears the rows it reads
+          for (int q = lane; q < (2 + 2 * R) * (RP / 4); q += 32)
+            reinterpret_cast<float4*>(stage + (2 * warp) * RP)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          fence_proxy_async();
+          __syncwarp();
+        } else if (MODE != VKT_BORDER && edge) {
+          // repair the out-of-volume cells of this warp's read window
+          fixup_f32<MODE, R>(stage, plane_ptr<float>(p, src), p, x0, y0, lane, 32, 2 * warp,
+                             2 * warp + 2 + 2 * R);
+          fence_proxy_async();
+          __syncwarp();
+        }
+      }
+    } else {
+      // refill the raw slot of plane i-1 (converted two iterations ago)
+      if (i >= 1 && i - 1 + SR < np) {
+        mbar_wait(&raw_free[(i - 1) % SR], (uint32_t)(((i - 1) / SR) & 1));
+        issue(i - 1 + SR);
+      }
+      if (i + C::AHEAD < np) prepare(i + C::AHEAD);
+      mbar_wait(&ready[s], (uint32_t)((i / S) & 1));
     }
-
-    // slot m <-> output plane zo0 + i - 2R + m (chunk-relative i - 2R + m)
-    const int first = 2 * R - i;          // first valid slot
-    const int last = nzo - 1 - i + 2 * R;  // last valid slot
+    // slot m <-> output plane zo0 + i - 2R + m
+    const int first = 2 * R - i;
+    const int last = nzo - 1 - i + 2 * R;
     if (first <= 0 && last >= K - 1)
-      plane_step<T, K, false>(stage, tx, ty, wt, acc, 0, K - 1);
+      plane_step<K, false>(stage, tx, ty, wt, acc, 0, K - 1);
     else
-      plane_step<T, K, true>(stage, tx, ty, wt, acc, first, last);
+      plane_step<K, true>(stage, tx, ty, wt, acc, first, last);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
 
-    if (i >= 2 * R && out_ok) {
+    if (i >= 2 * R && valid > 0) {
       const int oz = zo0 + i - 2 * R;
-      store4<T>(out_base + (int64_t)oz * plane_elems, acc[0], p.c);
+      store8<T>(out_base + (int64_t)oz * plane_elems, acc[0], p.c, valid);
     }
 #pragma unroll
     for (int m = 0; m < K - 1; ++m)
@@ -361,22 +546,20 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int j = 0; j < XPT; ++j) acc[m][j] = acc[m + 1][j];
 #pragma unroll
     for (int j = 0; j < XPT; ++j) acc[K - 1][j] = 0.0f;
-
-    __syncthreads();  // stage s is free for plane i + STAGES
-    if (tid == 0) fence_proxy_async();
   }
 }
 
 template <typename T, int K, int MODE>
 cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, const CUtensorMap& mh,
                               const TmaParams& p, const float* w32, dim3 grid, cudaStream_t s) {
-  using G = Geo<T, K / 2>;
-  Weights<K> wt;
-  for (int i = 0; i < K * K * K; ++i) wt.w[i] = w32[i];
+  using C = Cfg<T, K>;
+  Weights<K> wt = {};
+  for (int r = 0; r < K * K; ++r)
+    for (int x = 0; x < K; ++x) wt.w[r * Weights<K>::KP + x] = w32[r * K + x];
   auto fn = filter_tma_kernel<T, K, MODE>;
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (err != cudaSuccess) return err;
-  fn<<<grid, THREADS, G::SMEM, s>>>(ms, ml, mh, p, wt);
+  fn<<<grid, THREADS, C::SMEM, s>>>(ms, ml, mh, p, wt);
   return cudaGetLastError();
 }
 

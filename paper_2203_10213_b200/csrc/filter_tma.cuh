@@ -37,10 +37,25 @@ namespace vkt {
 namespace tma {
 
 constexpr int TX = 128;          // outputs per CTA in x
-constexpr int XPT = 8;           // outputs per compute thread in x
-constexpr int WARPS = 8;         // 2 CTAs/SM -> 4 warps per SMSP -> 128 registers
-constexpr int TY = WARPS * 32 / (TX / XPT);  // 16 output rows per CTA
-constexpr int THREADS = 32 * WARPS;
+constexpr int TY = 16;           // outputs per CTA in y
+constexpr int XPT = 8;           // outputs per thread in x
+
+// Thread layout per kernel extent (measured):
+//  K <= 5: 2 output rows per thread (each weight load feeds 16 FFMAs), 4 warps,
+//          3 CTAs/SM (3 warps per SMSP, 168 registers);
+//  K == 7: 1 row per thread (the 2-row variant needs 112 accumulators and
+//          loses latency hiding), 8 warps, 2 CTAs/SM (4 warps/SMSP, 128 regs).
+// Warps per SM stay a multiple of 4 so every SM sub-partition gets the same
+// number of FMA warps.
+template <int K>
+struct Layout {
+  static constexpr int YPT = K <= 5 ? 2 : 1;
+  static constexpr int WARPS = TY * (TX / XPT) / (32 * YPT);
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int CTAS_PER_SM = K <= 5 ? 3 : 2;
+  static constexpr int WROWS = TY / WARPS;  // output rows per warp
+  static constexpr int SMEM_PER_CTA = (228 * 1024) / CTAS_PER_SM - 1024;  // minus driver reserve
+};
 constexpr int RP = TX + 8;       // ready-stage row pitch (floats): x in [x0-4, x0+TX+4)
 
 // Raw TMA box geometry (shared by the host tensor-map encode and the kernel).
@@ -55,6 +70,7 @@ __host__ __device__ constexpr int box_width(int r, int bpc) {
 
 template <typename T, int K>
 struct Cfg {
+  using L = Layout<K>;
   static constexpr int R = K / 2;
   static constexpr bool IS_F32 = sizeof(T) == 4;
   static constexpr int A = box_align_left(R, (int)sizeof(T));
@@ -64,16 +80,21 @@ struct Cfg {
   static constexpr int RAW_PITCH = (RAW_BYTES + 127) / 128 * 128;
   static constexpr int RDY_BYTES = RP * BY * 4;
   static constexpr int RDY_PITCH = (RDY_BYTES + 127) / 128 * 128;
-  // ready-ring depth (f32: TMA lands here directly, so it is also the TMA
-  // lookahead; small K needs more planes in flight to cover HBM latency)
-  static constexpr int S_RDY = IS_F32 ? (K == 3 ? 10 : K == 5 ? 6 : 5) : 4;
-  static constexpr int S_RAW = IS_F32 ? 0 : (K == 3 ? 10 : K == 5 ? 6 : 5);
+  // Ring depths: as deep as fits CTAS_PER_SM CTAs per SM (f32: the TMA lands
+  // in the ready ring, so it is also the TMA lookahead; ints: 4 ready stages
+  // and the rest of the budget as raw TMA stages), capped at 10.
+  static constexpr int BUDGET = L::SMEM_PER_CTA - 512;
+  static constexpr int S_RDY = IS_F32 ? (BUDGET / RDY_PITCH < 10 ? BUDGET / RDY_PITCH : 10) : 4;
+  static constexpr int S_RAW_FIT = IS_F32 ? 0 : (BUDGET - 4 * RDY_PITCH) / RAW_PITCH;
+  static constexpr int S_RAW = IS_F32 ? 0 : (S_RAW_FIT < 10 ? S_RAW_FIT : 10);
   static constexpr int AHEAD = 2;  // ints: planes converted ahead of compute
   static constexpr int SMEM_DATA = S_RDY * RDY_PITCH + S_RAW * RAW_PITCH;
   static constexpr int NBAR = 2 * S_RDY + 2 * (IS_F32 ? S_RDY : S_RAW);
   static constexpr int SMEM = SMEM_DATA + NBAR * 8 + 128;
   static_assert(!IS_F32 || BX == RP, "f32 TMA box must match the ready layout");
   static_assert(R >= 1 && R <= 4, "radius");
+  static_assert(IS_F32 ? S_RDY >= 4 : S_RAW >= 4, "ring too shallow");
+  static_assert(SMEM <= L::SMEM_PER_CTA, "shared memory budget");
   static_assert(BX <= 256 && BY <= 256, "TMA box too large");
 };
 
@@ -351,25 +372,31 @@ __device__ __forceinline__ void store8<uint8_t>(uint8_t* out, const float (&a)[X
                                                    q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24)));
 }
 
-// One input plane's contribution to the K rolling accumulators of 8 outputs.
-// GUARD: skip slots whose output plane is outside the chunk (ramp up/down).
+// One input plane's contribution to the K rolling accumulators of the
+// thread's 2 x 8 outputs (rows 2*ty and 2*ty+1).  GUARD: skip slots whose
+// output plane is outside the chunk (ramp up / down).
 template <int K, bool GUARD>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage, int tx, int ty,
-                                           const Weights<K>& wt, float (&acc)[K][XPT], int first,
+                                           const Weights<K>& wt,
+                                           float (&acc)[Layout<K>::YPT][K][XPT], int first,
                                            int last) {
+  constexpr int YPT = Layout<K>::YPT;
   constexpr int R = K / 2;
   constexpr int OFF = 4 - R;
 #pragma unroll(K <= 3 ? K : 1)
   for (int dy = 0; dy < K; ++dy) {
-    const float4* row = reinterpret_cast<const float4*>(stage + (ty + dy) * RP + XPT * tx);
-    float v[16];
+    float v[YPT][16];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 q = row[i];
-      v[4 * i + 0] = q.x;
-      v[4 * i + 1] = q.y;
-      v[4 * i + 2] = q.z;
-      v[4 * i + 3] = q.w;
+    for (int r = 0; r < YPT; ++r) {
+      const float4* row = reinterpret_cast<const float4*>(stage + (YPT * ty + r + dy) * RP + XPT * tx);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 q = row[i];
+        v[r][4 * i + 0] = q.x;
+        v[r][4 * i + 1] = q.y;
+        v[r][4 * i + 2] = q.z;
+        v[r][4 * i + 3] = q.w;
+      }
     }
 #pragma unroll
     for (int m = 0; m < K; ++m) {
@@ -380,14 +407,16 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage, int 
       for (int dx = 0; dx < K; ++dx) {
         const float wv = w[dx];
 #pragma unroll
-        for (int j = 0; j < XPT; ++j) acc[m][j] = __fmaf_rn(wv, v[OFF + j + dx], acc[m][j]);
+        for (int r = 0; r < YPT; ++r)
+#pragma unroll
+          for (int j = 0; j < XPT; ++j) acc[r][m][j] = __fmaf_rn(wv, v[r][OFF + j + dx], acc[r][m][j]);
       }
     }
   }
 }
 
 template <typename T, int K, int MODE>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
     filter_tma_kernel(const __grid_constant__ CUtensorMap map_src,
                       const __grid_constant__ CUtensorMap map_lo,
                       const __grid_constant__ CUtensorMap map_hi, const TmaParams p,
@@ -395,6 +424,10 @@ __global__ void __launch_bounds__(THREADS, 2)
   using C = Cfg<T, K>;
   constexpr int R = C::R;
   constexpr int S = C::S_RDY;
+  constexpr int YPT = Layout<K>::YPT;
+  constexpr int WARPS = Layout<K>::WARPS;
+  constexpr int THREADS = Layout<K>::THREADS;
+  constexpr int WROWS = Layout<K>::WROWS;
   constexpr int SR = C::IS_F32 ? C::S_RDY : C::S_RAW;  // TMA ring depth
   extern __shared__ __align__(128) uint8_t smem_raw[];
   // TMA destinations must be 128-byte aligned; do not rely on the base.
@@ -478,15 +511,19 @@ __global__ void __launch_bounds__(THREADS, 2)
 
   const int tx = tid % (TX / XPT);
   const int ty = tid / (TX / XPT);
-  float acc[K][XPT];
+  float acc[YPT][K][XPT];
 #pragma unroll
-  for (int m = 0; m < K; ++m)
+  for (int r = 0; r < YPT; ++r)
 #pragma unroll
-    for (int j = 0; j < XPT; ++j) acc[m][j] = 0.0f;
+    for (int m = 0; m < K; ++m)
+#pragma unroll
+      for (int j = 0; j < XPT; ++j) acc[r][m][j] = 0.0f;
 
   const int ox = x0 + tx * XPT;
-  const int oy = y0 + ty;
-  const int valid = (oy < p.ny) ? min(XPT, p.nx - ox) : 0;
+  const int oy = y0 + YPT * ty;
+  int valid[YPT];
+#pragma unroll
+  for (int r = 0; r < YPT; ++r) valid[r] = (oy + r < p.ny) ? min(XPT, p.nx - ox) : 0;
   T* out_base = static_cast<T*>(p.dst) + (int64_t)oy * p.nx + ox;
   const int64_t plane_elems = (int64_t)p.nx * p.ny;
 
@@ -505,14 +542,14 @@ __global__ void __launch_bounds__(THREADS, 2)
         const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + i);
         if (src.which < 0) {
           // Border zero plane: this warp clears the rows it reads
-          for (int q = lane; q < (2 + 2 * R) * (RP / 4); q += 32)
-            reinterpret_cast<float4*>(stage + (2 * warp) * RP)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = lane; q < (WROWS + 2 * R) * (RP / 4); q += 32)
+            reinterpret_cast<float4*>(stage + (WROWS * warp) * RP)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           fence_proxy_async();
           __syncwarp();
         } else if (MODE != VKT_BORDER && edge) {
           // repair the out-of-volume cells of this warp's read window
-          fixup_f32<MODE, R>(stage, plane_ptr<float>(p, src), p, x0, y0, lane, 32, 2 * warp,
-                             2 * warp + 2 + 2 * R);
+          fixup_f32<MODE, R>(stage, plane_ptr<float>(p, src), p, x0, y0, lane, 32, WROWS * warp,
+                             WROWS * warp + WROWS + 2 * R);
           fence_proxy_async();
           __syncwarp();
         }
@@ -536,16 +573,22 @@ __global__ void __launch_bounds__(THREADS, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
-    if (i >= 2 * R && valid > 0) {
+    if (i >= 2 * R) {
       const int oz = zo0 + i - 2 * R;
-      store8<T>(out_base + (int64_t)oz * plane_elems, acc[0], p.c, valid);
+#pragma unroll
+      for (int r = 0; r < YPT; ++r)
+        if (valid[r] > 0)
+          store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.nx, acc[r][0], p.c, valid[r]);
     }
 #pragma unroll
-    for (int m = 0; m < K - 1; ++m)
+    for (int r = 0; r < YPT; ++r) {
 #pragma unroll
-      for (int j = 0; j < XPT; ++j) acc[m][j] = acc[m + 1][j];
+      for (int m = 0; m < K - 1; ++m)
 #pragma unroll
-    for (int j = 0; j < XPT; ++j) acc[K - 1][j] = 0.0f;
+        for (int j = 0; j < XPT; ++j) acc[r][m][j] = acc[r][m + 1][j];
+#pragma unroll
+      for (int j = 0; j < XPT; ++j) acc[r][K - 1][j] = 0.0f;
+    }
   }
 }
 
@@ -559,7 +602,7 @@ cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, cons
   auto fn = filter_tma_kernel<T, K, MODE>;
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (err != cudaSuccess) return err;
-  fn<<<grid, THREADS, C::SMEM, s>>>(ms, ml, mh, p, wt);
+  fn<<<grid, Layout<K>::THREADS, C::SMEM, s>>>(ms, ml, mh, p, wt);
   return cudaGetLastError();
 }
 

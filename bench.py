@@ -302,6 +302,13 @@ def run_ours(args):
                            f"(sm_max_mhz, {peak_src}); hbm: {hbm_gbs} GB/s {peak_src}")
     roof["kernel_ms"] = round(kern_ms, 4)
     roof["kernel_path"] = vk.filter_path(dst.local, src.local, kernel)
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists() and world == 1 and roof["kernel_path"] == "tma":
+        ent = json.loads(tf.read_text()).get("filter_tma_kernel<u16,7,clamp> 1024^3")
+        if ent:
+            roof["traffic"] = ent["total_bytes"]
+            roof["traffic_note"] = (f"dram read+write per launch from {ent['capture']} "
+                                    f"(algorithmic {ent['algorithmic_bytes']} B)")
 
     extra = None
     if world == 1 and not args.no_extra:

@@ -100,6 +100,21 @@ typedef struct {
 /* ApplyFilter: dst = correlate(src, weights) re-quantized (filters.py:69-95). */
 int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream);
 
+/* ApplyFilter on HOST buffers, streamed through HBM (the reference's
+ * apply_filter works on host numpy arrays, filters.py:69-95).
+ *   args->src / args->dst: HOST pointers to planes [z_offset, z_offset+dims.z)
+ *   of a volume with global_nz planes (0 => dims.z, z_offset 0: the whole
+ *   volume); page-locked memory gives copy/compute overlap.  Computes the
+ *   output planes [out_z_begin, out_z_end) of the buffer (default: all) by
+ *   uploading z-chunks of `chunk_planes` planes plus their address-mapped
+ *   halo planes (which must lie inside the buffer), filtering each chunk
+ *   with the device path and downloading it, with H2D / compute / D2H
+ *   overlapped on three streams.  Results are bit-identical to
+ *   vkt_apply_filter on the whole volume.  Volumes larger than HBM work (only
+ *   3 chunks are resident).  Returns when dst holds the result.
+ *   halo_lo / halo_hi must be NULL. */
+int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_planes, vkt_stream_t stream);
+
 /* Which kernel vkt_apply_filter would launch for these args (VKT_PATH_*). */
 int vkt_filter_path(const vkt_filter_args* args);
 

@@ -35,6 +35,7 @@ from .filters import (
     Filter,
     Kernel,
     apply_filter,
+    apply_filter_host,
     box_kernel,
     filter_path,
     gaussian_kernel,
@@ -58,7 +59,8 @@ __all__ = [
     "AddressMode", "AllocationFailure", "ApplyFilter", "Box3i", "DataFormat", "Device",
     "DeviceBuffer", "DeviceFailure", "DimsMismatch", "EvenKernelDims", "ExecutionPolicy",
     "Fill", "FillRange", "Filter", "FilterPath", "IndexOutOfRange", "InvalidArgument", "Kernel",
-    "StructuredVolume", "Vec3f", "Vec3i", "VktError", "VoxelMapping", "apply_filter", "box3i",
+    "StructuredVolume", "Vec3f", "Vec3i", "VktError", "VoxelMapping", "apply_filter",
+    "apply_filter_host", "box3i",
     "box_kernel", "clip_box", "create_structured_volume", "dequantize_scalar", "errors", "fill",
     "fill_range", "filter_path", "full_box", "gaussian_kernel", "get_execution_policy",
     "laplacian_kernel", "quantize_scalar", "set_execution_policy", "synthetic_device",

@@ -26,6 +26,7 @@ PATH_NAMES = {PATH_NONE: "none", PATH_DIRECT: "direct", PATH_EXACT: "exact", PAT
 
 EXPORTED_SYMBOLS = (
     "vkt_apply_filter",
+    "vkt_apply_filter_host",
     "vkt_filter_path",
     "vkt_fill_box",
     "vkt_fill_synthetic",
@@ -82,6 +83,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
                                   ctypes.c_uint32, ctypes.c_uint64)
         lib.vkt_apply_filter.argtypes = [ctypes.POINTER(FilterArgs), vp]
         lib.vkt_apply_filter.restype = ctypes.c_int
+        lib.vkt_apply_filter_host.argtypes = [ctypes.POINTER(FilterArgs), ctypes.c_int32, vp]
+        lib.vkt_apply_filter_host.restype = ctypes.c_int
         lib.vkt_filter_path.argtypes = [ctypes.POINTER(FilterArgs)]
         lib.vkt_filter_path.restype = ctypes.c_int
         lib.vkt_fill_box.argtypes = [vp, Int3, i32, Int3, Int3, u32, vp]

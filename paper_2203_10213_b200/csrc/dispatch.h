@@ -22,6 +22,12 @@ struct FilterPlan {
 
 void set_error_detail(const char* fmt, ...);
 
+// Stream-ordered scratch from a library-owned memory pool on the current
+// device whose release threshold is unlimited, so repeated calls reuse the
+// same HBM instead of mapping/unmapping it on every synchronize.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+cudaError_t scratch_free(void* p, cudaStream_t s);
+
 int launch_filter_direct(const FilterPlan& plan, cudaStream_t s);
 // Returns VKT_OK, an error, or -1 when the tiled kernel does not cover `plan`.
 int launch_filter_tma(const FilterPlan& plan, cudaStream_t s);

@@ -134,9 +134,9 @@ int launch_filter_direct(const FilterPlan& plan, cudaStream_t s) {
   // on different streams never share device state.
   size_t bytes = ntaps * (exact ? sizeof(double) : sizeof(float));
   void* dw = nullptr;
-  cudaError_t err = cudaMallocAsync(&dw, bytes, s);
+  cudaError_t err = scratch_alloc(&dw, bytes, s);
   if (err != cudaSuccess) {
-    set_error_detail("cudaMallocAsync(weights): %s", cudaGetErrorString(err));
+    set_error_detail("scratch_alloc(weights): %s", cudaGetErrorString(err));
     return err == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
   }
   if (exact)
@@ -144,7 +144,7 @@ int launch_filter_direct(const FilterPlan& plan, cudaStream_t s) {
   else
     err = cudaMemcpyAsync(dw, plan.w32.data(), bytes, cudaMemcpyHostToDevice, s);
   if (err != cudaSuccess) {
-    cudaFreeAsync(dw, s);
+    scratch_free(dw, s);
     set_error_detail("cudaMemcpyAsync(weights): %s", cudaGetErrorString(err));
     return VKT_DEVICE_FAILURE;
   }
@@ -173,7 +173,7 @@ int launch_filter_direct(const FilterPlan& plan, cudaStream_t s) {
     case VKT_U16: err = launch_direct_mode<uint16_t>(p, a.address_mode, exact, s); break;
     default: err = launch_direct_mode<float>(p, a.address_mode, exact, s); break;
   }
-  cudaFreeAsync(dw, s);
+  scratch_free(dw, s);
   if (err != cudaSuccess) {
     set_error_detail("filter_direct launch: %s", cudaGetErrorString(err));
     return VKT_DEVICE_FAILURE;

@@ -115,7 +115,7 @@ int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
   const int nzo = plan.z_end - plan.z_begin;
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
   int zc = 64;
-  while (zc > 8 && nxy * ((nzo + zc - 1) / zc) < 148 * 8) zc /= 2;
+  while (zc > 16 && nxy * ((nzo + zc - 1) / zc) < 148 * 4) zc /= 2;
   if (zc > nzo) zc = nzo;
   p.zc = zc;
   dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + tma::TY - 1) / tma::TY,

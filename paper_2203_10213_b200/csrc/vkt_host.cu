@@ -1,0 +1,219 @@
+// vkt_host.cu — ApplyFilter on host buffers, streamed through HBM.
+//
+// The reference filters host numpy arrays (filters.py:69-95).  This entry
+// point keeps that contract for callers whose volume lives in host memory:
+// it cuts the requested output planes into z-chunks, and for each chunk
+//   H2D  : uploads the chunk's planes plus its 2*rz halo planes (address
+//          mapped at the global z boundary, zero planes for Border) into one
+//          contiguous device buffer [halo_lo | slab | halo_hi],
+//   GPU  : runs the device ApplyFilter on the slab with those halos — the
+//          same sharded-slab machinery as the multi-GPU path, so results are
+//          bit-identical to a whole-volume launch,
+//   D2H  : downloads the chunk's output planes,
+// with the three phases of consecutive chunks overlapped on three streams
+// and NB buffer sets in rotation.  Only NB chunks are resident, so volumes
+// larger than HBM work.
+#include <algorithm>
+#include <vector>
+
+#include "dispatch.h"
+
+namespace vkt {
+namespace {
+
+constexpr int NB = 3;  // buffer sets in flight
+
+// Owns the pipeline's streams, events and device pool; on every exit path
+// (including errors) it drains the streams before releasing anything, so no
+// copy can still be reading or writing the caller's host buffers.
+struct HostCtx {
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_comp = nullptr;
+  cudaEvent_t h2d_done[NB] = {}, comp_done[NB] = {}, d2h_done[NB] = {}, alloc_done = nullptr;
+  uint8_t* pool = nullptr;
+  ~HostCtx() {
+    if (s_h2d) cudaStreamSynchronize(s_h2d);
+    if (s_d2h) cudaStreamSynchronize(s_d2h);
+    if (s_comp) cudaStreamSynchronize(s_comp);
+    if (pool) {
+      scratch_free(pool, s_comp);
+      cudaStreamSynchronize(s_comp);
+    }
+    for (int b = 0; b < NB; ++b) {
+      if (h2d_done[b]) cudaEventDestroy(h2d_done[b]);
+      if (comp_done[b]) cudaEventDestroy(comp_done[b]);
+      if (d2h_done[b]) cudaEventDestroy(d2h_done[b]);
+    }
+    if (alloc_done) cudaEventDestroy(alloc_done);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
+  }
+};
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error_detail("%s: %s", what, cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
+}
+
+#define VKT_CK(call, what)                        \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+int64_t map_plane(int64_t g, int64_t n, int mode) {
+  switch (mode) {
+    case VKT_WRAP: return map_index<VKT_WRAP>(g, n);
+    case VKT_MIRROR: return map_index<VKT_MIRROR>(g, n);
+    case VKT_CLAMP: return map_index<VKT_CLAMP>(g, n);
+    default: return map_index<VKT_BORDER>(g, n);
+  }
+}
+
+// Upload global planes g0 .. g0+count-1 (address mapped over gnz) into dev,
+// merging runs of consecutive source planes into one copy; Border planes are
+// zeroed.  The host buffer holds global planes [hz0, hz0 + hnz).
+int upload_planes(uint8_t* dev, const uint8_t* host, int64_t hz0, int64_t hnz, int64_t g0,
+                  int count, int64_t gnz, int64_t plane_bytes, int mode, cudaStream_t s) {
+  int i = 0;
+  while (i < count) {
+    const int64_t m = map_plane(g0 + i, gnz, mode);
+    int run = 1;
+    if (m < 0) {
+      while (i + run < count && map_plane(g0 + i + run, gnz, mode) < 0) ++run;
+      VKT_CK(cudaMemsetAsync(dev + (int64_t)i * plane_bytes, 0, run * plane_bytes, s), "memset halo");
+    } else {
+      if (m < hz0 || m >= hz0 + hnz) {
+        set_error_detail("plane %lld needed for the halo is not in the host buffer [%lld, %lld)",
+                         (long long)m, (long long)hz0, (long long)(hz0 + hnz));
+        return VKT_INVALID_ARGUMENT;
+      }
+      while (i + run < count && map_plane(g0 + i + run, gnz, mode) == m + run &&
+             m + run < hz0 + hnz)
+        ++run;
+      VKT_CK(cudaMemcpyAsync(dev + (int64_t)i * plane_bytes, host + (m - hz0) * plane_bytes,
+                             run * plane_bytes, cudaMemcpyHostToDevice, s),
+             "H2D chunk");
+    }
+    i += run;
+  }
+  return VKT_OK;
+}
+
+}  // namespace
+}  // namespace vkt
+
+using namespace vkt;
+
+extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_planes,
+                                     vkt_stream_t stream) {
+  if (args == nullptr) {
+    set_error_detail("args is NULL");
+    return VKT_INVALID_ARGUMENT;
+  }
+  const vkt_filter_args& a = *args;
+  if (a.halo_lo || a.halo_hi) {
+    set_error_detail("vkt_apply_filter_host resolves halos itself (halo_lo/halo_hi must be NULL)");
+    return VKT_INVALID_ARGUMENT;
+  }
+  const int64_t gnz = a.global_nz > 0 ? a.global_nz : a.dims.z;
+  if (a.z_offset < 0 || a.z_offset + a.dims.z > gnz) {
+    set_error_detail("host slab [%lld, %lld) outside global z extent %lld", (long long)a.z_offset,
+                     (long long)(a.z_offset + a.dims.z), (long long)gnz);
+    return VKT_INVALID_ARGUMENT;
+  }
+  // Validate everything except the device pointers with the device-path
+  // planner, using placeholder device addresses.
+  {
+    vkt_filter_args probe = a;
+    probe.src = reinterpret_cast<const void*>(uintptr_t(256));
+    probe.dst = reinterpret_cast<void*>(uintptr_t(512));
+    probe.z_offset = 0;
+    probe.global_nz = 0;
+    if (a.src == nullptr || a.dst == nullptr) {
+      set_error_detail("src and dst must be non-NULL host pointers");
+      return VKT_INVALID_ARGUMENT;
+    }
+    if (vkt_filter_path(&probe) == VKT_PATH_NONE) return vkt_apply_filter(&probe, nullptr);
+  }
+  cudaStream_t s_comp = reinterpret_cast<cudaStream_t>(stream);
+  const int bpc = a.format == VKT_U8 ? 1 : a.format == VKT_U16 ? 2 : 4;
+  const int64_t nz = a.dims.z;  // planes in the host buffers
+  const int64_t plane_bytes = (int64_t)a.dims.x * a.dims.y * bpc;
+  const int rz = a.kdims.z / 2;
+  const int zb = a.out_z_begin > 0 ? a.out_z_begin : 0;
+  const int ze = a.out_z_end > 0 ? std::min<int>(a.out_z_end, (int)nz) : (int)nz;
+  if (ze <= zb) return VKT_OK;
+  // default chunk: ~128 MB of planes (long enough for full-depth z chunks in
+  // the kernel and few launches, short enough to fill the pipeline quickly)
+  int C = chunk_planes > 0 ? chunk_planes : (int)std::max<int64_t>(16, (128ll << 20) / plane_bytes);
+  C = std::min(C, ze - zb);
+
+  HostCtx ctx;
+  ctx.s_comp = s_comp;
+  VKT_CK(cudaStreamCreateWithFlags(&ctx.s_h2d, cudaStreamNonBlocking), "stream");
+  VKT_CK(cudaStreamCreateWithFlags(&ctx.s_d2h, cudaStreamNonBlocking), "stream");
+  for (int b = 0; b < NB; ++b) {
+    VKT_CK(cudaEventCreateWithFlags(&ctx.h2d_done[b], cudaEventDisableTiming), "event");
+    VKT_CK(cudaEventCreateWithFlags(&ctx.comp_done[b], cudaEventDisableTiming), "event");
+    VKT_CK(cudaEventCreateWithFlags(&ctx.d2h_done[b], cudaEventDisableTiming), "event");
+  }
+  VKT_CK(cudaEventCreateWithFlags(&ctx.alloc_done, cudaEventDisableTiming), "event");
+
+  // NB x ([rz | C | rz] input planes + C output planes), stream-ordered.
+  const int64_t in_bytes = (int64_t)(C + 2 * rz) * plane_bytes;
+  const int64_t out_bytes = (int64_t)C * plane_bytes;
+  const int64_t set_bytes = ((in_bytes + 255) / 256 + (out_bytes + 255) / 256) * 256;
+  VKT_CK(scratch_alloc(reinterpret_cast<void**>(&ctx.pool), NB * set_bytes, s_comp),
+         "scratch_alloc");
+  uint8_t* pool = ctx.pool;
+  VKT_CK(cudaEventRecord(ctx.alloc_done, s_comp), "event");
+  VKT_CK(cudaStreamWaitEvent(ctx.s_h2d, ctx.alloc_done, 0), "wait");
+  VKT_CK(cudaStreamWaitEvent(ctx.s_d2h, ctx.alloc_done, 0), "wait");
+
+  const uint8_t* hsrc = static_cast<const uint8_t*>(a.src);
+  uint8_t* hdst = static_cast<uint8_t*>(a.dst);
+  int status = VKT_OK;
+  int c = 0;
+  for (int z0 = zb; z0 < ze && status == VKT_OK; z0 += C, ++c) {
+    const int z1 = std::min(z0 + C, ze);
+    const int n = z1 - z0;
+    const int b = c % NB;
+    uint8_t* in = pool + b * set_bytes;
+    uint8_t* out = in + (in_bytes + 255) / 256 * 256;
+    if (c >= NB) VKT_CK(cudaStreamWaitEvent(ctx.s_h2d, ctx.d2h_done[b], 0), "wait");
+    // [halo_lo | slab | halo_hi] = global planes [z0-rz, z1+rz) address-mapped
+    status = upload_planes(in, hsrc, a.z_offset, nz, a.z_offset + z0 - rz, n + 2 * rz, gnz,
+                           plane_bytes, a.address_mode, ctx.s_h2d);
+    if (status != VKT_OK) break;
+    VKT_CK(cudaEventRecord(ctx.h2d_done[b], ctx.s_h2d), "event");
+
+    VKT_CK(cudaStreamWaitEvent(s_comp, ctx.h2d_done[b], 0), "wait");
+    vkt_filter_args ca = a;
+    ca.src = in + (int64_t)rz * plane_bytes;
+    ca.dst = out;
+    ca.dims.z = n;
+    ca.halo_lo = rz > 0 ? in : nullptr;
+    ca.halo_hi = rz > 0 ? in + (int64_t)(rz + n) * plane_bytes : nullptr;
+    ca.z_offset = a.z_offset + z0;
+    ca.global_nz = gnz;
+    ca.out_z_begin = 0;
+    ca.out_z_end = 0;
+    status = vkt_apply_filter(&ca, reinterpret_cast<vkt_stream_t>(s_comp));
+    if (status != VKT_OK) break;
+    VKT_CK(cudaEventRecord(ctx.comp_done[b], s_comp), "event");
+
+    VKT_CK(cudaStreamWaitEvent(ctx.s_d2h, ctx.comp_done[b], 0), "wait");
+    VKT_CK(cudaMemcpyAsync(hdst + (int64_t)z0 * plane_bytes, out, (int64_t)n * plane_bytes,
+                           cudaMemcpyDeviceToHost, ctx.s_d2h),
+           "D2H chunk");
+    VKT_CK(cudaEventRecord(ctx.d2h_done[b], ctx.s_d2h), "event");
+  }
+  // drain (the pool is released by ~HostCtx after the last download)
+  cudaError_t e1 = cudaStreamSynchronize(ctx.s_h2d);
+  cudaError_t e2 = cudaStreamSynchronize(ctx.s_d2h);
+  cudaError_t e3 = cudaStreamSynchronize(s_comp);
+  if (status != VKT_OK) return status;
+  for (cudaError_t e : {e1, e2, e3})
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline");
+  return VKT_OK;
+}

@@ -231,3 +231,53 @@ def apply_filter(volume: StructuredVolume, kernel: Kernel, address_mode=AddressM
     if not isinstance(kernel, Kernel):
         raise InvalidArgument("kernel must be a Kernel")
     _apply_in_place(volume, kernel, AddressMode.coerce(address_mode))
+
+
+def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *, fmt=None,
+                      mapping=(0.0, 1.0), out=None, z_range=None, chunk_planes: int = 0,
+                      z_offset: int = 0, global_nz: int = 0):
+    """ApplyFilter on a HOST (z, y, x) array, streamed through HBM.
+
+    The reference filters host numpy arrays (filters.py:69-95); this keeps that
+    contract without a device-resident volume: ``vkt_apply_filter_host``
+    uploads z-chunks plus their halo planes, filters and downloads them with
+    the three phases overlapped (page-locked arrays, e.g. numpy views of
+    ``torch.empty(..., pin_memory=True)``, make the copies asynchronous).
+    Returns ``out`` (a new array of the input dtype unless given); only the
+    output planes ``z_range`` (default all) are written.  Bit-identical to
+    ``ApplyFilter`` on the whole volume; volumes larger than HBM work.
+
+    ``z_offset`` / ``global_nz``: the array holds global planes
+    [z_offset, z_offset + nz) of a volume with ``global_nz`` planes (a z-slab
+    read with range I/O, or one rank's share); every halo plane the requested
+    outputs need must be inside it.  ``z_range`` is relative to the array.
+    """
+    import torch
+
+    if not isinstance(kernel, Kernel):
+        raise InvalidArgument("kernel must be a Kernel")
+    src = np.asarray(stored)
+    if src.ndim != 3 or not src.flags["C_CONTIGUOUS"]:
+        raise InvalidArgument("apply_filter_host needs a C-contiguous (z, y, x) array")
+    if fmt is None:
+        fmt = {np.dtype("<u1"): DataFormat.UINT8, np.dtype("<u2"): DataFormat.UINT16,
+               np.dtype("<f4"): DataFormat.FLOAT32}.get(src.dtype.newbyteorder("<") if src.dtype.byteorder == ">" else src.dtype)
+        if fmt is None:
+            raise InvalidArgument(f"no voxel format for dtype {src.dtype}")
+    fmt = fmt if isinstance(fmt, DataFormat) else DataFormat.parse(fmt)
+    if src.dtype != fmt.dtype:
+        raise InvalidArgument(f"array dtype {src.dtype} does not match format {fmt.short_name}")
+    if out is None:
+        out = np.empty_like(src)
+    elif out.shape != src.shape or out.dtype != src.dtype or not out.flags["C_CONTIGUOUS"]:
+        raise InvalidArgument("out must match the input's shape and dtype and be C-contiguous")
+    nz, ny, nx = src.shape
+    zb, ze = (0, 0) if z_range is None else (int(z_range[0]), int(z_range[1]))
+    mode = AddressMode.coerce(address_mode)
+    args, _keep = make_args(out.ctypes.data, src.ctypes.data, (nx, ny, nz), fmt, mapping, kernel, mode,
+                            out_z_begin=zb, out_z_end=ze, z_offset=z_offset, global_nz=global_nz,
+                            flags=_flags(get_execution_policy()))
+    stream = int(torch.cuda.current_stream().cuda_stream) if torch.cuda.is_available() else 0
+    _capi.check(_capi.load().vkt_apply_filter_host(ctypes.byref(args), int(chunk_planes),
+                                                   ctypes.c_void_p(stream)))
+    return out

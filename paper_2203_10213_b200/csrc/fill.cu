@@ -23,6 +23,34 @@ struct FillParams {
 
 static constexpr int64_t kFillChunk = 32768;  // bytes per CTA work item
 
+// Short segments (partial rows of a FillRange box): one warp per segment.
+__global__ void __launch_bounds__(256) fill_rows_kernel(FillParams p) {
+  const int64_t nseg = p.n_seg_y * p.n_seg_z;
+  const uint4 vec = make_uint4(p.pattern, p.pattern, p.pattern, p.pattern);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t seg = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; seg < nseg; seg += warps) {
+    const int64_t sy = seg % p.n_seg_y;
+    const int64_t sz = seg / p.n_seg_y;
+    uint8_t* lo = p.base + sz * p.stride_z + sy * p.stride_y;
+    uint8_t* hi = lo + p.seg_bytes;
+    uint8_t* vlo = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lo) + 15) & ~uintptr_t(15));
+    uint8_t* vhi = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(hi) & ~uintptr_t(15));
+    if (vlo > vhi) { vlo = hi; vhi = hi; }
+    const int64_t head_cells = (vlo - lo) / p.bpc;
+    const int64_t tail_cells = (hi - vhi) / p.bpc;
+    for (int64_t i = lane; i < head_cells + tail_cells; i += 32) {
+      uint8_t* c = i < head_cells ? lo + i * p.bpc : vhi + (i - head_cells) * p.bpc;
+      if (p.bpc == 1) *c = (uint8_t)p.pattern;
+      else if (p.bpc == 2) *reinterpret_cast<uint16_t*>(c) = (uint16_t)p.pattern;
+      else *reinterpret_cast<uint32_t*>(c) = p.pattern;
+    }
+    uint4* v = reinterpret_cast<uint4*>(vlo);
+    const int64_t nv = (vhi - vlo) / 16;
+    for (int64_t i = lane; i < nv; i += 32) __stcs(v + i, vec);
+  }
+}
+
 __global__ void __launch_bounds__(256) fill_box_kernel(FillParams p) {
   const int64_t items = p.n_seg_y * p.n_seg_z * p.chunks_per_seg;
   const uint4 vec = make_uint4(p.pattern, p.pattern, p.pattern, p.pattern);
@@ -95,8 +123,14 @@ int launch_fill_box(void* dst, vkt_int3 dims, int format, vkt_int3 lo, vkt_int3 
   p.stride_z = plane_b;
   p.chunks_per_seg = (p.seg_bytes + kFillChunk - 1) / kFillChunk;
   const int64_t items = p.n_seg_y * p.n_seg_z * p.chunks_per_seg;
-  int grid = (int)(items < 148 * 16 ? items : 148 * 16);
-  fill_box_kernel<<<grid, 256, 0, s>>>(p);
+  if (p.seg_bytes <= 4096) {
+    const int64_t nseg = p.n_seg_y * p.n_seg_z;
+    const int64_t blocks = (nseg + 7) / 8;
+    fill_rows_kernel<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(p);
+  } else {
+    int grid = (int)(items < 148 * 16 ? items : 148 * 16);
+    fill_box_kernel<<<grid, 256, 0, s>>>(p);
+  }
   count_launch();
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {

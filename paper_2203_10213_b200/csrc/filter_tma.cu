@@ -110,13 +110,24 @@ int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
   p.global_nz = plan.geom.global_nz;
   p.c = plan.epi_c;
 
-  // Chunk depth: long enough to amortise the 2R-plane z halo of a chunk,
-  // short enough for >= ~8 CTAs per SM worth of work items (tail effect).
+  // Chunk depth ZC: every CTA pays ~2R extra input planes plus a pipeline
+  // fill; the grid pays wave quantization.  Pick the ZC with the smallest
+  // estimated time  waves(ZC) * (ZC + 2R + fill)  (fill ~ 3 planes).
   const int nzo = plan.z_end - plan.z_begin;
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
+  const int64_t slots = 148ll * (k == 7 ? tma::Layout<7>::CTAS_PER_SM : tma::Layout<3>::CTAS_PER_SM);
   int zc = 64;
-  while (zc > 16 && nxy * ((nzo + zc - 1) / zc) < 148 * 4) zc /= 2;
-  if (zc > nzo) zc = nzo;
+  double best = 1e300;
+  for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {
+    const int z = cand < nzo ? cand : nzo;
+    const int64_t ctas = nxy * ((nzo + z - 1) / z);
+    const int64_t waves = (ctas + slots - 1) / slots;
+    const double cost = (double)waves * (z + 2 * r + 3);
+    if (cost < best * 0.98) {
+      best = cost;
+      zc = z;
+    }
+  }
   p.zc = zc;
   dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + tma::TY - 1) / tma::TY,
             (nzo + zc - 1) / zc);

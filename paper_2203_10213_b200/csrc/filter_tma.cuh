@@ -305,6 +305,12 @@ __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T*
   constexpr int R = C::R;
   constexpr int QPR = RP / 4;  // quads per row
   constexpr int NQ = QPR * C::BY;
+  // in-volume window of this tile in stage coordinates (row by <-> y0-R+by,
+  // ready index e <-> x0-4+e); cells outside it may need repair
+  const int oob_rows_lo = max(0, R - y0);
+  const int oob_rows_hi = p.ny - y0 + R;
+  const int oob_x_lo = max(0, 4 - x0);
+  const int oob_x_hi = p.nx - x0 + 4;
 #pragma unroll 2
   for (int q = t; q < NQ; q += nt) {
     const int by = q / QPR;
@@ -324,7 +330,10 @@ __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T*
       f[2] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7442)) - 8388608.0f;
       f[3] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7443)) - 8388608.0f;
     }
-    if (MODE != VKT_BORDER && edge) {
+    // only quads that hold out-of-volume cells of the read window take the
+    // per-cell path: rows outside [0, ny) or columns outside [0, nx)
+    if (MODE != VKT_BORDER && edge &&
+        (by < oob_rows_lo || by >= oob_rows_hi || e < oob_x_lo || e + 4 > oob_x_hi)) {
       const int gy = y0 - R + by;
       const bool yo = gy < 0 || gy >= p.ny;
 #pragma unroll

@@ -157,6 +157,21 @@ def exchange_halos(plan: HaloPlan, rank: int, local_planes, halo_lo, halo_hi, gr
         w.wait()
 
 
+def exchange_halos_host_staged(plan: HaloPlan, rank: int, local_planes, halo_lo, halo_hi,
+                               group=None) -> None:
+    """``exchange_halos`` for backends without device P2P (gloo): the planes
+    this rank sends are staged to host memory, exchanged, and the received
+    halos copied back.  Used by the multi-process tests that run several ranks
+    on one GPU, where NCCL's spinning P2P kernels must not share a device."""
+    sends, recvs, _local, _zeros = plan.for_rank(rank)
+    need = sorted({(t.src_first, t.count) for t in sends})
+    host_planes = local_planes.cpu() if need else local_planes[:0].cpu()
+    h_lo, h_hi = halo_lo.cpu(), halo_hi.cpu()
+    exchange_halos(plan, rank, host_planes, h_lo, h_hi, group)
+    halo_lo.copy_(h_lo)
+    halo_hi.copy_(h_hi)
+
+
 class ShardedVolume:
     """This rank's z-slab of a global volume, plus its halo buffers."""
 

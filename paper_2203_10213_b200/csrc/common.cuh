@@ -125,27 +125,36 @@ struct FormatTraits<float> {
 };
 
 // ----------------------------------------------------------------------------
-// Epilogue (fast path): S = sum w_f32 * s_f32 in stored units.
+// Epilogue (fast path).  S = sum w_f32 * s_f32 in stored units, accumulated in
+// the (dz, dy, dx) tap order.
 // Ints: t*max = S + c with c = lo*(sum_w - 1)/(hi - lo)*max computed in f64 on
-// the host (SURVEY §8(c) "Epilogue restatement"); out = floor(clamp(.)+0.5).
-// F32 volumes store S verbatim (quantize() is astype('<f4'), volume.py:106).
+// the host (SURVEY §8(c) "Epilogue restatement"), out = floor(clamp(.)+0.5).
+// The accumulator STARTS at acc0 = fl(c + 0.5), so the epilogue is a
+// saturating floor conversion (negatives -> 0) and one integer min.
+// F32 volumes start at 0 and store the sum verbatim (quantize() is
+// astype('<f4'), volume.py:106).  Every kernel path uses these two helpers,
+// so all paths stay bit-identical.
 // ----------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ T quantize_f32(float S, float c);
+__host__ __device__ __forceinline__ float acc_init(float c) {
+  if constexpr (FormatTraits<T>::is_int) return c + 0.5f;
+  else return 0.0f;
+}
+
+template <typename T>
+__device__ __forceinline__ T quantize_acc(float acc);
 
 template <>
-__device__ __forceinline__ uint8_t quantize_f32<uint8_t>(float S, float c) {
-  float y = fminf(fmaxf(S + c, 0.0f), 255.0f);
-  return (uint8_t)__float2uint_rd(y + 0.5f);
+__device__ __forceinline__ uint8_t quantize_acc<uint8_t>(float acc) {
+  return (uint8_t)min(__float2uint_rd(acc), 255u);
 }
 template <>
-__device__ __forceinline__ uint16_t quantize_f32<uint16_t>(float S, float c) {
-  float y = fminf(fmaxf(S + c, 0.0f), 65535.0f);
-  return (uint16_t)__float2uint_rd(y + 0.5f);
+__device__ __forceinline__ uint16_t quantize_acc<uint16_t>(float acc) {
+  return (uint16_t)min(__float2uint_rd(acc), 65535u);
 }
 template <>
-__device__ __forceinline__ float quantize_f32<float>(float S, float) {
-  return S;
+__device__ __forceinline__ float quantize_acc<float>(float acc) {
+  return acc;
 }
 
 // Launch accounting (see vkt_launch_count).

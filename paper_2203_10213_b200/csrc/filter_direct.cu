@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) filter_direct_kernel(DirectParams p) {
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= p.nx || y >= p.ny) return;
   for (int z = p.z_begin + blockIdx.z; z < p.z_end; z += gridDim.z) {
-    float acc = 0.0f;
+    float acc = acc_init<T>(p.c);
     int t = 0;
     for (int dz = 0; dz < p.kz; ++dz) {
       const T* plane = resolve_plane<MODE, T>(p.g, z + dz - p.g.rz);
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) filter_direct_kernel(DirectParams p) {
       }
     }
     T* out = static_cast<T*>(p.dst) + ((int64_t)z * p.ny + y) * p.nx + x;
-    *out = quantize_f32<T>(acc, p.c);
+    *out = quantize_acc<T>(acc);
   }
 }
 

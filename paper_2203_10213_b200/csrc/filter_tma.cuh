@@ -293,28 +293,72 @@ __device__ __forceinline__ void fixup_f32(float* stage, const float* plane, cons
   }
 }
 
-// u8/u16: widen this thread's share of the raw TMA plane into the ready stage
-// (layout: x from x0-4).  On edge tiles the out-of-volume cells are replaced
-// by their address-mapped value, read from the raw stage (Clamp / Mirror) or
-// gathered from global memory (Wrap); Border keeps the TMA zero fill.
-template <typename T, int MODE, int K>
+// u8/u16: this thread's share of the widening work, fixed for the whole CTA
+// (the tile geometry is the same for every plane): quad q = t + k*nt covers
+// ready cells [e, e+4) of stage row `by`.  Offsets are computed once; `slow`
+// marks quads that hold out-of-volume cells of the read window.
+template <typename T, int K, int NT>
+struct QuadPlan {
+  using C = Cfg<T, K>;
+  static constexpr int QPR = RP / 4;  // quads per row
+  static constexpr int NQ = QPR * C::BY;
+  static constexpr int QPT = (NQ + NT - 1) / NT;
+  // K = 7 runs at the 128-register budget: recompute instead of storing.
+  static constexpr bool STORE = K <= 5;
+  int rdy_[STORE ? QPT : 1];  // ready-stage float offset (-1: no quad)
+  uint32_t slow_;             // bit k: quad k takes the per-cell edge path
+  int t_, rows_lo_, rows_hi_, x_lo_, x_hi_;
+  bool edge_;
+
+  __device__ __forceinline__ QuadPlan(const TmaParams& p, int x0, int y0, bool edge, int t) {
+    constexpr int R = C::R;
+    t_ = t;
+    edge_ = edge;
+    rows_lo_ = max(0, R - y0);
+    rows_hi_ = p.ny - y0 + R;
+    x_lo_ = max(0, 4 - x0);
+    x_hi_ = p.nx - x0 + 4;
+    slow_ = 0;
+    if constexpr (STORE) {
+#pragma unroll
+      for (int k = 0; k < QPT; ++k) {
+        int ro;
+        bool sl;
+        compute(k, ro, sl);
+        rdy_[k] = ro;
+        slow_ |= (sl ? 1u : 0u) << k;
+      }
+    }
+  }
+  __device__ __forceinline__ void compute(int k, int& ro, bool& sl) const {
+    const int q = t_ + k * NT;
+    const int by = q / QPR, e = (q - by * QPR) * 4;
+    ro = q < NQ ? by * RP + e : -1;
+    sl = q < NQ && edge_ && (by < rows_lo_ || by >= rows_hi_ || e < x_lo_ || e + 4 > x_hi_);
+  }
+  __device__ __forceinline__ void get(int k, int& ro, bool& sl) const {
+    if constexpr (STORE) {
+      ro = rdy_[k];
+      sl = (slow_ >> k) & 1u;
+    } else {
+      compute(k, ro, sl);
+    }
+  }
+};
+
+template <typename T, int MODE, int K, int NT>
 __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T* plane,
-                                              const TmaParams& p, int x0, int y0, bool edge, int t,
-                                              int nt) {
+                                              const TmaParams& p, int x0, int y0,
+                                              const QuadPlan<T, K, NT>& qp) {
   using C = Cfg<T, K>;
   constexpr int R = C::R;
-  constexpr int QPR = RP / 4;  // quads per row
-  constexpr int NQ = QPR * C::BY;
-  // in-volume window of this tile in stage coordinates (row by <-> y0-R+by,
-  // ready index e <-> x0-4+e); cells outside it may need repair
-  const int oob_rows_lo = max(0, R - y0);
-  const int oob_rows_hi = p.ny - y0 + R;
-  const int oob_x_lo = max(0, 4 - x0);
-  const int oob_x_hi = p.nx - x0 + 4;
-#pragma unroll 2
-  for (int q = t; q < NQ; q += nt) {
-    const int by = q / QPR;
-    const int e = (q - by * QPR) * 4;  // ready index of the quad's first cell
+#pragma unroll
+  for (int k = 0; k < QuadPlan<T, K, NT>::QPT; ++k) {
+    int ro;
+    bool sl;
+    qp.get(k, ro, sl);
+    if (ro < 0) continue;
+    const int by = ro / RP, e = ro - by * RP;
     const T* src = raw + by * C::BX + e + (C::A - 4);
     float f[4];
     if constexpr (sizeof(T) == 2) {
@@ -330,10 +374,7 @@ __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T*
       f[2] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7442)) - 8388608.0f;
       f[3] = __int_as_float(__byte_perm(w, 0x4B000000u, 0x7443)) - 8388608.0f;
     }
-    // only quads that hold out-of-volume cells of the read window take the
-    // per-cell path: rows outside [0, ny) or columns outside [0, nx)
-    if (MODE != VKT_BORDER && edge &&
-        (by < oob_rows_lo || by >= oob_rows_hi || e < oob_x_lo || e + 4 > oob_x_hi)) {
+    if (MODE != VKT_BORDER && sl) {
       const int gy = y0 - R + by;
       const bool yo = gy < 0 || gy >= p.ny;
 #pragma unroll
@@ -349,7 +390,7 @@ __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T*
         }
       }
     }
-    *reinterpret_cast<float4*>(rdy + by * RP + e) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(rdy + ro) = make_float4(f[0], f[1], f[2], f[3]);
   }
 }
 
@@ -357,26 +398,26 @@ __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T*
 // Compute helpers
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void store8(T* out, const float (&a)[XPT], float c, int valid);
+__device__ __forceinline__ void store8(T* out, const float (&a)[XPT], int valid);
 
 template <>
-__device__ __forceinline__ void store8<float>(float* out, const float (&a)[XPT], float, int valid) {
+__device__ __forceinline__ void store8<float>(float* out, const float (&a)[XPT], int valid) {
   if (valid >= 4) __stcs(reinterpret_cast<float4*>(out), make_float4(a[0], a[1], a[2], a[3]));
   if (valid >= 8) __stcs(reinterpret_cast<float4*>(out) + 1, make_float4(a[4], a[5], a[6], a[7]));
 }
 template <>
-__device__ __forceinline__ void store8<uint16_t>(uint16_t* out, const float (&a)[XPT], float c, int) {
+__device__ __forceinline__ void store8<uint16_t>(uint16_t* out, const float (&a)[XPT], int) {
   uint32_t q[XPT];
 #pragma unroll
-  for (int j = 0; j < XPT; ++j) q[j] = quantize_f32<uint16_t>(a[j], c);
+  for (int j = 0; j < XPT; ++j) q[j] = quantize_acc<uint16_t>(a[j]);
   __stcs(reinterpret_cast<uint4*>(out),
          make_uint4(q[0] | (q[1] << 16), q[2] | (q[3] << 16), q[4] | (q[5] << 16), q[6] | (q[7] << 16)));
 }
 template <>
-__device__ __forceinline__ void store8<uint8_t>(uint8_t* out, const float (&a)[XPT], float c, int) {
+__device__ __forceinline__ void store8<uint8_t>(uint8_t* out, const float (&a)[XPT], int) {
   uint32_t q[XPT];
 #pragma unroll
-  for (int j = 0; j < XPT; ++j) q[j] = quantize_f32<uint8_t>(a[j], c);
+  for (int j = 0; j < XPT; ++j) q[j] = quantize_acc<uint8_t>(a[j]);
   __stcs(reinterpret_cast<uint2*>(out), make_uint2(q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24),
                                                    q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24)));
 }
@@ -491,7 +532,8 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
                  s.z, leader);
   };
 
-  // ints: widen plane j (all warps, 1/8 share each) into ready stage j % S.
+  // ints: widen plane j (all warps, equal shares) into ready stage j % S.
+  const QuadPlan<T, K, THREADS> qplan(p, x0, y0, edge, tid);
   auto prepare = [&](int j) {
     const int s = j % S;
     float* stage = rdy_base + s * (C::RDY_PITCH / 4);
@@ -504,7 +546,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
       for (int q = tid; q < C::RDY_BYTES / 16; q += THREADS) w4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
       const T* raw = raw_base + r * (C::RAW_PITCH / (int)sizeof(T));
-      convert_plane<T, MODE, K>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, edge, tid, THREADS);
+      convert_plane<T, MODE, K, THREADS>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, qplan);
     }
     __syncwarp();
     if (lane == 0) {
@@ -520,13 +562,14 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
 
   const int tx = tid % (TX / XPT);
   const int ty = tid / (TX / XPT);
+  const float a0 = acc_init<T>(p.c);
   float acc[YPT][K][XPT];
 #pragma unroll
   for (int r = 0; r < YPT; ++r)
 #pragma unroll
     for (int m = 0; m < K; ++m)
 #pragma unroll
-      for (int j = 0; j < XPT; ++j) acc[r][m][j] = 0.0f;
+      for (int j = 0; j < XPT; ++j) acc[r][m][j] = a0;
 
   const int ox = x0 + tx * XPT;
   const int oy = y0 + YPT * ty;
@@ -587,7 +630,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
 #pragma unroll
       for (int r = 0; r < YPT; ++r)
         if (valid[r] > 0)
-          store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.nx, acc[r][0], p.c, valid[r]);
+          store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.nx, acc[r][0], valid[r]);
     }
 #pragma unroll
     for (int r = 0; r < YPT; ++r) {
@@ -596,7 +639,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
 #pragma unroll
         for (int j = 0; j < XPT; ++j) acc[r][m][j] = acc[r][m + 1][j];
 #pragma unroll
-      for (int j = 0; j < XPT; ++j) acc[r][K - 1][j] = 0.0f;
+      for (int j = 0; j < XPT; ++j) acc[r][K - 1][j] = a0;
     }
   }
 }

@@ -101,18 +101,21 @@ typedef struct {
 int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream);
 
 /* ApplyFilter on HOST buffers, streamed through HBM (the reference's
- * apply_filter works on host numpy arrays, filters.py:69-95).
- *   args->src / args->dst: HOST pointers to planes [z_offset, z_offset+dims.z)
- *   of a volume with global_nz planes (0 => dims.z, z_offset 0: the whole
- *   volume); page-locked memory gives copy/compute overlap.  Computes the
- *   output planes [out_z_begin, out_z_end) of the buffer (default: all) by
- *   uploading z-chunks of `chunk_planes` planes plus their address-mapped
- *   halo planes (which must lie inside the buffer), filtering each chunk
- *   with the device path and downloading it, with H2D / compute / D2H
- *   overlapped on three streams.  Results are bit-identical to
- *   vkt_apply_filter on the whole volume.  Volumes larger than HBM work (only
- *   3 chunks are resident).  Returns when dst holds the result.
- *   halo_lo / halo_hi must be NULL. */
+ * apply_filter works on host numpy arrays, filters.py:69-95).  Same argument
+ * meaning as vkt_apply_filter with every pointer on the HOST:
+ *   src / dst : planes [z_offset, z_offset+dims.z) of a volume with
+ *               global_nz planes (0 => dims.z; z_offset 0: the whole volume);
+ *   halo_lo / halo_hi : optional, rz planes each = the address-mapped global
+ *               planes z_offset-rz .. z_offset-1 and after the buffer; when
+ *               NULL every halo plane must map inside the buffer (always true
+ *               for a whole volume).
+ * Computes output planes [out_z_begin, out_z_end) of the buffer (default
+ * all) by uploading z-chunks of `chunk_planes` planes (0: ~128 MB) plus their
+ * halo planes, filtering each chunk with the device path and downloading
+ * it, with H2D / compute / D2H overlapped on three streams; page-locked
+ * buffers make the copies asynchronous.  Bit-identical to vkt_apply_filter on
+ * the whole volume.  Only 3 chunks are resident, so volumes larger than HBM
+ * work.  Returns when dst holds the result. */
 int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_planes, vkt_stream_t stream);
 
 /* Which kernel vkt_apply_filter would launch for these args (VKT_PATH_*). */

@@ -129,7 +129,24 @@ def main():
         fills[f"f{i:02d}/output"] = v.array().copy()
         fills[f"f{i:02d}/spec"] = np.array([fmt, mapping[0], mapping[1], *lower, *upper, value])
     np.savez_compressed(OUT / "fill_cases.npz", **fills)
-    print(f"wrote {idx} filter cases, {len(specs)} fill cases to {OUT}")
+
+    # VKTVOL01 files written by the reference (io.py:164-194) and the output
+    # of the reference CLI `vkt filter` on them (cli.py:359-375)
+    import subprocess
+    vrng = np.random.default_rng(5)
+    for fmt, dims, mapping, cell in ((1, (20, 12, 9), (0.0, 1.0), (1.0, 1.0, 1.0)),
+                                    (2, (16, 8, 11), (-1.0, 3.0), (0.5, 1.0, 2.0)),
+                                    (3, (12, 10, 7), (0.0, 1.0), (1.0, 1.0, 1.0))):
+        v = vkt.StructuredVolume(dims, FMTS[fmt], cell, mapping)
+        v.array()[...] = random_stored(vrng, dims, fmt)
+        name = f"vol_{FMTS[fmt].short_name}.vkt"
+        vkt.write_volume(OUT / name, v)
+        out = subprocess.run([sys.executable, "-m", "vkt", "filter", "--gaussian", "1.0", "--ksize", "3",
+                              "-i", str(OUT / name), "-o", str(OUT / f"filtered_{name}")],
+                             env={**__import__("os").environ, "PYTHONPATH": "/root/reference/pkg/src"},
+                             capture_output=True)
+        assert out.returncode == 0, out.stderr
+    print(f"wrote {idx} filter cases, {len(specs)} fill cases, 3 VKTVOL01 files to {OUT}")
 
 
 if __name__ == "__main__":

@@ -12,8 +12,16 @@ behind the C ABI in include/vkt_b200.h.  There is no CPU fallback.
 from . import errors
 from .errors import (
     AllocationFailure,
+    BadMagic,
     DeviceFailure,
     DimsMismatch,
+    EmptyRange,
+    IoFailure,
+    NotSeekable,
+    RangeOutOfBounds,
+    SizeMismatch,
+    TruncatedPayload,
+    UnknownFormatCode,
     EvenKernelDims,
     IndexOutOfRange,
     InvalidArgument,
@@ -52,6 +60,16 @@ from .volume import (
     quantize_scalar,
 )
 from .synthetic import synthetic_device, synthetic_host, synthetic_structured
+from .io import (
+    filter_file,
+    load_raw,
+    read_range,
+    read_volume,
+    volume_from_bytes,
+    volume_to_bytes,
+    write_range,
+    write_volume,
+)
 
 __version__ = "0.1.0"
 
@@ -65,4 +83,6 @@ __all__ = [
     "fill_range", "filter_path", "full_box", "gaussian_kernel", "get_execution_policy",
     "laplacian_kernel", "quantize_scalar", "set_execution_policy", "synthetic_device",
     "synthetic_host", "synthetic_structured", "timed", "with_policy",
+    "filter_file", "load_raw", "read_range", "read_volume", "volume_from_bytes", "volume_to_bytes",
+    "write_range", "write_volume",
 ]

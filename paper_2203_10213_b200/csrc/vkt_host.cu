@@ -69,14 +69,42 @@ int64_t map_plane(int64_t g, int64_t n, int mode) {
   }
 }
 
-// Upload global planes g0 .. g0+count-1 (address mapped over gnz) into dev,
-// merging runs of consecutive source planes into one copy; Border planes are
-// zeroed.  The host buffer holds global planes [hz0, hz0 + hnz).
-int upload_planes(uint8_t* dev, const uint8_t* host, int64_t hz0, int64_t hnz, int64_t g0,
-                  int count, int64_t gnz, int64_t plane_bytes, int mode, cudaStream_t s) {
+struct HostSlab {
+  const uint8_t* buf;      // global planes [z0, z0 + n)
+  int64_t z0, n;
+  const uint8_t* halo_lo;  // mapped planes for g in [z0 - rz, z0), or NULL
+  const uint8_t* halo_hi;  // mapped planes for g in [z0 + n, z0 + n + rz), or NULL
+  int rz;
+};
+
+// Upload global planes g0 .. g0+count-1 into dev: planes inside the host
+// buffer are copied directly, planes in the caller's halo ranges come from
+// the host halos, everything else is address mapped over gnz (Border planes
+// are zeroed).  Runs of consecutive source planes become one copy.
+int upload_planes(uint8_t* dev, const HostSlab& h, int64_t g0, int count, int64_t gnz,
+                  int64_t plane_bytes, int mode, cudaStream_t s) {
   int i = 0;
   while (i < count) {
-    const int64_t m = map_plane(g0 + i, gnz, mode);
+    const int64_t g = g0 + i;
+    const uint8_t* halo = nullptr;
+    int64_t hidx = 0;
+    if (g < h.z0 && h.halo_lo != nullptr && g >= h.z0 - h.rz) {
+      halo = h.halo_lo;
+      hidx = g - (h.z0 - h.rz);
+    } else if (g >= h.z0 + h.n && h.halo_hi != nullptr && g < h.z0 + h.n + h.rz) {
+      halo = h.halo_hi;
+      hidx = g - (h.z0 + h.n);
+    }
+    if (halo != nullptr) {
+      VKT_CK(cudaMemcpyAsync(dev + (int64_t)i * plane_bytes, halo + hidx * plane_bytes, plane_bytes,
+                             cudaMemcpyHostToDevice, s),
+             "H2D halo");
+      i += 1;
+      continue;
+    }
+    const int64_t hz0 = h.z0, hnz = h.n;
+    const uint8_t* host = h.buf;
+    const int64_t m = map_plane(g, gnz, mode);
     int run = 1;
     if (m < 0) {
       while (i + run < count && map_plane(g0 + i + run, gnz, mode) < 0) ++run;
@@ -88,7 +116,7 @@ int upload_planes(uint8_t* dev, const uint8_t* host, int64_t hz0, int64_t hnz, i
         return VKT_INVALID_ARGUMENT;
       }
       while (i + run < count && map_plane(g0 + i + run, gnz, mode) == m + run &&
-             m + run < hz0 + hnz)
+             m + run < hz0 + hnz && g0 + i + run >= hz0 && g0 + i + run < hz0 + hnz)
         ++run;
       VKT_CK(cudaMemcpyAsync(dev + (int64_t)i * plane_bytes, host + (m - hz0) * plane_bytes,
                              run * plane_bytes, cudaMemcpyHostToDevice, s),
@@ -111,10 +139,6 @@ extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_
     return VKT_INVALID_ARGUMENT;
   }
   const vkt_filter_args& a = *args;
-  if (a.halo_lo || a.halo_hi) {
-    set_error_detail("vkt_apply_filter_host resolves halos itself (halo_lo/halo_hi must be NULL)");
-    return VKT_INVALID_ARGUMENT;
-  }
   const int64_t gnz = a.global_nz > 0 ? a.global_nz : a.dims.z;
   if (a.z_offset < 0 || a.z_offset + a.dims.z > gnz) {
     set_error_detail("host slab [%lld, %lld) outside global z extent %lld", (long long)a.z_offset,
@@ -129,6 +153,8 @@ extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_
     probe.dst = reinterpret_cast<void*>(uintptr_t(512));
     probe.z_offset = 0;
     probe.global_nz = 0;
+    probe.halo_lo = nullptr;
+    probe.halo_hi = nullptr;
     if (a.src == nullptr || a.dst == nullptr) {
       set_error_detail("src and dst must be non-NULL host pointers");
       return VKT_INVALID_ARGUMENT;
@@ -182,8 +208,10 @@ extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_
     uint8_t* out = in + (in_bytes + 255) / 256 * 256;
     if (c >= NB) VKT_CK(cudaStreamWaitEvent(ctx.s_h2d, ctx.d2h_done[b], 0), "wait");
     // [halo_lo | slab | halo_hi] = global planes [z0-rz, z1+rz) address-mapped
-    status = upload_planes(in, hsrc, a.z_offset, nz, a.z_offset + z0 - rz, n + 2 * rz, gnz,
-                           plane_bytes, a.address_mode, ctx.s_h2d);
+    const HostSlab hs{hsrc, a.z_offset, nz, static_cast<const uint8_t*>(a.halo_lo),
+                      static_cast<const uint8_t*>(a.halo_hi), rz};
+    status = upload_planes(in, hs, a.z_offset + z0 - rz, n + 2 * rz, gnz, plane_bytes,
+                           a.address_mode, ctx.s_h2d);
     if (status != VKT_OK) break;
     VKT_CK(cudaEventRecord(ctx.h2d_done[b], ctx.s_h2d), "event");
 

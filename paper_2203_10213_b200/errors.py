@@ -37,6 +37,38 @@ class DimsMismatch(VktError):
     """Operand volumes disagree in dimensions, format or mapping (errors.py:49)."""
 
 
+class EmptyRange(VktError):
+    """The region of interest selects no cells (errors.py:37)."""
+
+
+class RangeOutOfBounds(VktError):
+    """The region of interest extends past the volume bounds (errors.py:41)."""
+
+
+class BadMagic(VktError):
+    """The stream does not start with VKTVOL01 (errors.py:57)."""
+
+
+class TruncatedPayload(VktError):
+    """The stream ends before the header-implied byte count (errors.py:61)."""
+
+
+class UnknownFormatCode(VktError):
+    """Unrecognised data-format or volume-type code (errors.py:65)."""
+
+
+class IoFailure(VktError):
+    """A read, write or flush failed (errors.py:69)."""
+
+
+class SizeMismatch(VktError):
+    """Raw payload length disagrees with the requested geometry (errors.py:73)."""
+
+
+class NotSeekable(VktError):
+    """Range I/O needs a seekable source (errors.py:77)."""
+
+
 class DeviceFailure(VktError):
     """The CUDA runtime reported an error, or no CUDA device / library exists.
 
@@ -48,7 +80,8 @@ class DeviceFailure(VktError):
 _BY_NAME = {
     cls.__name__: cls
     for cls in (InvalidArgument, IndexOutOfRange, AllocationFailure, EvenKernelDims,
-                DimsMismatch, DeviceFailure)
+                DimsMismatch, DeviceFailure, EmptyRange, RangeOutOfBounds, BadMagic,
+                TruncatedPayload, UnknownFormatCode, IoFailure, SizeMismatch, NotSeekable)
 }
 
 

@@ -235,7 +235,7 @@ def apply_filter(volume: StructuredVolume, kernel: Kernel, address_mode=AddressM
 
 def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *, fmt=None,
                       mapping=(0.0, 1.0), out=None, z_range=None, chunk_planes: int = 0,
-                      z_offset: int = 0, global_nz: int = 0):
+                      z_offset: int = 0, global_nz: int = 0, halo_lo=None, halo_hi=None):
     """ApplyFilter on a HOST (z, y, x) array, streamed through HBM.
 
     The reference filters host numpy arrays (filters.py:69-95); this keeps that
@@ -250,7 +250,9 @@ def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *,
     ``z_offset`` / ``global_nz``: the array holds global planes
     [z_offset, z_offset + nz) of a volume with ``global_nz`` planes (a z-slab
     read with range I/O, or one rank's share); every halo plane the requested
-    outputs need must be inside it.  ``z_range`` is relative to the array.
+    outputs need must be inside it, unless ``halo_lo`` / ``halo_hi`` (host
+    arrays of rz = kz//2 planes: the address-mapped planes just below and
+    above the array) supply them.  ``z_range`` is relative to the array.
     """
     import torch
 
@@ -274,9 +276,20 @@ def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *,
     nz, ny, nx = src.shape
     zb, ze = (0, 0) if z_range is None else (int(z_range[0]), int(z_range[1]))
     mode = AddressMode.coerce(address_mode)
+    halos = []
+    for h in (halo_lo, halo_hi):
+        if h is None:
+            halos.append(0)
+            continue
+        h = np.asarray(h)
+        if (h.dtype != src.dtype or not h.flags["C_CONTIGUOUS"]
+                or h.shape != (kernel.radius.z, ny, nx)):
+            raise InvalidArgument(f"halo arrays must be C-contiguous ({kernel.radius.z}, {ny}, {nx}) "
+                                  f"{src.dtype}")
+        halos.append(h.ctypes.data)
     args, _keep = make_args(out.ctypes.data, src.ctypes.data, (nx, ny, nz), fmt, mapping, kernel, mode,
                             out_z_begin=zb, out_z_end=ze, z_offset=z_offset, global_nz=global_nz,
-                            flags=_flags(get_execution_policy()))
+                            halo_lo=halos[0], halo_hi=halos[1], flags=_flags(get_execution_policy()))
     stream = int(torch.cuda.current_stream().cuda_stream) if torch.cuda.is_available() else 0
     _capi.check(_capi.load().vkt_apply_filter_host(ctypes.byref(args), int(chunk_planes),
                                                    ctypes.c_void_p(stream)))

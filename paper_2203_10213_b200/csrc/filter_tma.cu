@@ -54,7 +54,8 @@ int bpc_of(int format) { return format == VKT_U8 ? 1 : format == VKT_U16 ? 2 : 4
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int r) {
+bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int r,
+            int pitch) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return false;
   const int bpc = bpc_of(format);
@@ -62,7 +63,7 @@ bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz
                            : format == VKT_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
-  cuuint64_t strides[2] = {(cuuint64_t)nx * bpc, (cuuint64_t)nx * ny * bpc};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * bpc, (cuuint64_t)pitch * ny * bpc};
   cuuint32_t box[3] = {(cuuint32_t)tma::box_width(r, bpc), (cuuint32_t)(tma::TY + 2 * r), 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult res = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
@@ -78,32 +79,34 @@ bool tma_supported(const vkt_filter_args& a) {
   const int k = a.kdims.x;
   if (a.kdims.y != k || a.kdims.z != k) return false;
   if (k != 3 && k != 5 && k != 7) return false;
-  const int bpc = bpc_of(a.format);
-  if (((int64_t)a.dims.x * bpc) % 16 != 0) return false;  // TMA global stride rule
-  if (!aligned16(a.src) || !aligned16(a.dst)) return false;
-  if (a.halo_lo && !aligned16(a.halo_lo)) return false;
-  if (a.halo_hi && !aligned16(a.halo_hi)) return false;
+  // rows that are not 16-byte multiples (or unaligned buffers) are staged
+  // through pitched scratch copies (launch_filter_tma), so every extent works
   return encode_fn() != nullptr;
 }
 
-int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
+namespace {
+
+// Launch on buffers whose rows are `pitch` cells (16-byte multiple) apart.
+int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const void* hlo,
+                   const void* hhi, int pitch, cudaStream_t s) {
   const vkt_filter_args& a = *plan.args;
   const int k = a.kdims.x, r = k / 2;
   CUtensorMap ms, ml, mh;
-  if (!encode(&ms, a.src, a.format, a.dims.x, a.dims.y, a.dims.z, r)) return -1;
+  if (!encode(&ms, src, a.format, a.dims.x, a.dims.y, a.dims.z, r, pitch)) return -1;
   ml = ms;
   mh = ms;
-  if (a.halo_lo && r > 0 && !encode(&ml, a.halo_lo, a.format, a.dims.x, a.dims.y, r, r)) return -1;
-  if (a.halo_hi && r > 0 && !encode(&mh, a.halo_hi, a.format, a.dims.x, a.dims.y, r, r)) return -1;
+  if (hlo && r > 0 && !encode(&ml, hlo, a.format, a.dims.x, a.dims.y, r, r, pitch)) return -1;
+  if (hhi && r > 0 && !encode(&mh, hhi, a.format, a.dims.x, a.dims.y, r, r, pitch)) return -1;
 
   tma::TmaParams p{};
-  p.dst = a.dst;
-  p.src = a.src;
-  p.halo_lo = a.halo_lo;
-  p.halo_hi = a.halo_hi;
+  p.dst = dst;
+  p.src = src;
+  p.halo_lo = hlo;
+  p.halo_hi = hhi;
   p.nx = a.dims.x;
   p.ny = a.dims.y;
   p.nz = a.dims.z;
+  p.pitch = pitch;
   p.z_begin = plan.z_begin;
   p.z_end = plan.z_end;
   p.z_offset = plan.geom.z_offset;
@@ -151,6 +154,61 @@ int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
     return VKT_DEVICE_FAILURE;
   }
   return VKT_OK;
+}
+
+}  // namespace
+
+int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
+  const vkt_filter_args& a = *plan.args;
+  const int bpc = bpc_of(a.format);
+  const int rz = a.kdims.z / 2;
+  const bool direct = ((int64_t)a.dims.x * bpc) % 16 == 0 && aligned16(a.src) && aligned16(a.dst) &&
+                      (!a.halo_lo || aligned16(a.halo_lo)) && (!a.halo_hi || aligned16(a.halo_hi));
+  if (direct) return launch_pitched(plan, a.src, a.dst, a.halo_lo, a.halo_hi, a.dims.x, s);
+
+  // Pitched staging: copy the slab (and halos) into scratch with rows padded
+  // to 16 bytes, filter there, copy the computed planes back.  Two extra
+  // passes over the data; hidden for the FP32-bound kernels.
+  const int pitch = (int)((((int64_t)a.dims.x * bpc + 15) / 16 * 16) / bpc);
+  const size_t row_b = (size_t)a.dims.x * bpc, prow_b = (size_t)pitch * bpc;
+  const size_t pplane = prow_b * a.dims.y;
+  const int nzo = plan.z_end - plan.z_begin;
+  const size_t in_b = pplane * a.dims.z, halo_b = pplane * rz, out_b = pplane * nzo;
+  uint8_t* buf = nullptr;
+  const size_t total = in_b + 2 * halo_b + out_b + 64;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&buf), total, s);
+  if (e != cudaSuccess) {
+    set_error_detail("scratch_alloc(pitched staging, %zu bytes): %s", total, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
+  }
+  uint8_t* in = buf;
+  uint8_t* hlo = a.halo_lo ? in + in_b : nullptr;
+  uint8_t* hhi = a.halo_hi ? in + in_b + halo_b : nullptr;
+  uint8_t* out = in + in_b + 2 * halo_b;
+  auto copy2d = [&](void* d, size_t dp, const void* src, size_t sp, size_t rows) {
+    return cudaMemcpy2DAsync(d, dp, src, sp, row_b, rows, cudaMemcpyDeviceToDevice, s);
+  };
+  int st = VKT_OK;
+  if (copy2d(in, prow_b, a.src, row_b, (size_t)a.dims.y * a.dims.z) != cudaSuccess ||
+      (hlo && copy2d(hlo, prow_b, a.halo_lo, row_b, (size_t)a.dims.y * rz) != cudaSuccess) ||
+      (hhi && copy2d(hhi, prow_b, a.halo_hi, row_b, (size_t)a.dims.y * rz) != cudaSuccess)) {
+    set_error_detail("pitched staging copy: %s", cudaGetErrorString(cudaGetLastError()));
+    st = VKT_DEVICE_FAILURE;
+  }
+  if (st == VKT_OK) {
+    // the kernel addresses output plane oz at dst + oz * plane: shift so the
+    // computed planes [z_begin, z_end) land in `out`
+    uint8_t* dst_base = out - (ptrdiff_t)pplane * plan.z_begin;
+    st = launch_pitched(plan, in, dst_base, hlo, hhi, pitch, s);
+  }
+  if (st == VKT_OK &&
+      cudaMemcpy2DAsync(static_cast<uint8_t*>(a.dst) + row_b * a.dims.y * plan.z_begin, row_b, out, prow_b,
+                        row_b, (size_t)a.dims.y * nzo, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    set_error_detail("pitched staging copy back: %s", cudaGetErrorString(cudaGetLastError()));
+    st = VKT_DEVICE_FAILURE;
+  }
+  scratch_free(buf, s);
+  return st;
 }
 
 }  // namespace vkt

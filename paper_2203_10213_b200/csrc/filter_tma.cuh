@@ -121,6 +121,7 @@ struct TmaParams {
   const void* halo_lo;
   const void* halo_hi;
   int nx, ny, nz;        // local extents
+  int pitch;             // row pitch in cells (>= nx, rows 16-byte multiples)
   int z_begin, z_end;    // local output planes [begin, end)
   int zc;                // output planes per CTA chunk
   int64_t z_offset, global_nz;
@@ -213,7 +214,7 @@ __device__ __forceinline__ PlaneSrc resolve(const TmaParams& p, int R, int e) {
 
 template <typename T>
 __device__ __forceinline__ const T* plane_ptr(const TmaParams& p, PlaneSrc s) {
-  const int64_t pe = (int64_t)p.nx * p.ny;
+  const int64_t pe = (int64_t)p.pitch * p.ny;
   const void* base = s.which == 1 ? p.halo_lo : s.which == 2 ? p.halo_hi : p.src;
   return static_cast<const T*>(base) + (int64_t)s.z * pe;
 }
@@ -227,7 +228,7 @@ template <typename T, int MODE>
 __device__ __forceinline__ float gather_cell(const T* plane, const TmaParams& p, int gx, int gy) {
   const int mx = map_index32<MODE>(gx, p.nx);
   const int my = map_index32<MODE>(gy, p.ny);
-  return widen(__ldg(plane + (int64_t)my * p.nx + mx));
+  return widen(__ldg(plane + (int64_t)my * p.pitch + mx));
 }
 
 // ---------------------------------------------------------------------------
@@ -294,7 +295,7 @@ __device__ __forceinline__ void fixup_f32(float* stage, const float* plane, cons
         const int my = map_index32<MODE>(gy, p.ny);
         dst[b] = (gy - y0 + R) * RP + (gx - x0 + 4);
         if constexpr (MODE == VKT_WRAP)
-          val[b] = __ldg(plane + (int64_t)my * p.nx + mx);
+          val[b] = __ldg(plane + (int64_t)my * p.pitch + mx);
         else
           val[b] = stage[(my - y0 + R) * RP + (mx - x0 + 4)];
       }
@@ -396,7 +397,7 @@ __device__ __forceinline__ void convert_plane(float* rdy, const T* raw, const T*
           const int mx = map_index32<MODE>(gx, p.nx);
           const int my = map_index32<MODE>(gy, p.ny);
           if constexpr (MODE == VKT_WRAP)
-            f[c] = widen(__ldg(plane + (int64_t)my * p.nx + mx));
+            f[c] = widen(__ldg(plane + (int64_t)my * p.pitch + mx));
           else
             f[c] = widen(raw[(my - y0 + R) * C::BX + (mx - x0 + C::A)]);
         }
@@ -587,9 +588,10 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
   const int oy = y0 + YPT * ty;
   int valid[YPT];
 #pragma unroll
-  for (int r = 0; r < YPT; ++r) valid[r] = (oy + r < p.ny) ? min(XPT, p.nx - ox) : 0;
-  T* out_base = static_cast<T*>(p.dst) + (int64_t)oy * p.nx + ox;
-  const int64_t plane_elems = (int64_t)p.nx * p.ny;
+  // cells beyond nx up to the pitch are padding: storing there is harmless
+  for (int r = 0; r < YPT; ++r) valid[r] = (oy + r < p.ny) ? min(XPT, p.pitch - ox) : 0;
+  T* out_base = static_cast<T*>(p.dst) + (int64_t)oy * p.pitch + ox;
+  const int64_t plane_elems = (int64_t)p.pitch * p.ny;
 
   for (int i = 0; i < np; ++i) {
     const int s = i % S;
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
 #pragma unroll
       for (int r = 0; r < YPT; ++r)
         if (valid[r] > 0)
-          store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.nx, acc[r][0], valid[r]);
+          store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.pitch, acc[r][0], valid[r]);
     }
 #pragma unroll
     for (int r = 0; r < YPT; ++r) {

@@ -132,6 +132,35 @@ int vkt_fill_box(void* dst, vkt_int3 dims, int32_t format, vkt_int3 lo, vkt_int3
 int vkt_fill_synthetic(void* dst, vkt_int3 dims, int32_t format, uint64_t seed,
                        int64_t z_offset, vkt_stream_t stream);
 
+/* ---- CLAHE-3D (pkg/src/vkt/ops/filters.py:98-245) ----
+ * Brick partition, per-brick histograms, clipped-cdf mappings and the
+ * trilinear blend of the 8 nearest brick mappings.  The device computes the
+ * histograms (integer, exact) and the blend (IEEE float64 in the reference's
+ * operation order, bit-exact); the clip + cdf of the small per-brick
+ * histograms is host arithmetic. */
+typedef struct {
+  const void* src;        /* device volume                                        */
+  void* dst;              /* device volume (may equal src: each cell is read once) */
+  vkt_int3 dims;
+  int32_t format;
+  double map_lo, map_hi;
+  vkt_int3 bricks;        /* brick counts per axis                                */
+  int32_t num_bins;
+  const int32_t* bin_lut; /* device, u8/u16: stored value -> bin (host f64 rule);
+                             NULL for f32 (binned on the device in f64)           */
+  const int32_t* edges;   /* device, (bx+1)+(by+1)+(bz+1) brick edges x|y|z      */
+  uint32_t* hist;         /* device out (histograms): bz*by*bx*num_bins           */
+  const double* mappings; /* device in (blend): bz*by*bx*num_bins                  */
+  const int32_t* blend_lo;/* device in (blend): lower brick per cell, nx|ny|nz    */
+  const double* blend_w;  /* device in (blend): blend weight per cell,  nx|ny|nz  */
+} vkt_clahe_args;
+
+/* Per-brick histograms of the bin index min(nbins-1, floor(t*nbins)). */
+int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t stream);
+
+/* dst = quantize(lo + (sum of the 8 blended brick mappings)*(hi - lo)). */
+int vkt_clahe_blend(const vkt_clahe_args* args, vkt_stream_t stream);
+
 /* Error class name for a status code (errors.py naming). */
 const char* vkt_status_name(int status);
 

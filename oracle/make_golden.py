@@ -146,7 +146,34 @@ def main():
                              env={**__import__("os").environ, "PYTHONPATH": "/root/reference/pkg/src"},
                              capture_output=True)
         assert out.returncode == 0, out.stderr
-    print(f"wrote {idx} filter cases, {len(specs)} fill cases, 3 VKTVOL01 files to {OUT}")
+
+    # CLAHE-3D (filters.py:98-245): reference outputs and brick mappings
+    import math
+    crng = np.random.default_rng(2203)
+    clahe = {}
+    cspecs = [((16, 16, 16), 1, (0.0, 1.0), (2, 2, 2), 64, 3.0),
+              ((20, 12, 9), 1, (0.0, 1.0), (1, 1, 1), 256, math.inf),
+              ((17, 13, 11), 2, (-1.0, 3.0), (3, 2, 2), 128, 2.5),
+              ((12, 10, 7), 3, (0.0, 1.0), (2, 3, 1), 32, math.inf),
+              ((32, 32, 32), 1, (-1.0, 2.0), (2, 2, 2), 256, 4.0),
+              ((9, 21, 5), 3, (-0.5, 1.5), (2, 4, 3), 50, 1.0),
+              ((256, 1, 1), 1, (0.0, 1.0), (1, 1, 1), 256, math.inf)]
+    for i, (dims, fmt, mapping, bricks, bins, clip) in enumerate(cspecs):
+        stored = random_stored(crng, dims, fmt)
+        if i == len(cspecs) - 1:
+            stored = np.arange(256, dtype=np.uint8).reshape(1, 1, 256)
+        v = vkt.StructuredVolume(dims, FMTS[fmt], (1, 1, 1), mapping)
+        v.array()[...] = stored
+        params = vkt.ClaheParams(bricks, bins, clip)
+        from vkt.ops.filters import brick_mappings
+        maps = brick_mappings(v, params)
+        vkt.clahe_equalize(v, params)
+        clahe[f"h{i:02d}/input"] = stored
+        clahe[f"h{i:02d}/output"] = v.array().copy()
+        clahe[f"h{i:02d}/maps"] = maps
+        clahe[f"h{i:02d}/spec"] = np.array([fmt, mapping[0], mapping[1], *bricks, bins, clip])
+    np.savez_compressed(OUT / "clahe_cases.npz", **clahe)
+    print(f"wrote {idx} filter cases, {len(specs)} fill cases, 3 VKTVOL01 files, {len(cspecs)} CLAHE cases to {OUT}")
 
 
 if __name__ == "__main__":

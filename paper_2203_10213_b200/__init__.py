@@ -36,6 +36,7 @@ from .execution import (
     timed,
     with_policy,
 )
+from .clahe import ClaheParams, brick_mappings, clahe_equalize
 from .fill import Fill, FillRange, fill, fill_range
 from .filters import (
     AddressMode,
@@ -84,5 +85,5 @@ __all__ = [
     "laplacian_kernel", "quantize_scalar", "set_execution_policy", "synthetic_device",
     "synthetic_host", "synthetic_structured", "timed", "with_policy",
     "filter_file", "load_raw", "read_range", "read_volume", "volume_from_bytes", "volume_to_bytes",
-    "write_range", "write_volume",
+    "write_range", "write_volume", "ClaheParams", "brick_mappings", "clahe_equalize",
 ]

@@ -34,6 +34,8 @@ EXPORTED_SYMBOLS = (
     "vkt_last_error_detail",
     "vkt_launch_count",
     "vkt_abi_version",
+    "vkt_clahe_histograms",
+    "vkt_clahe_blend",
 )
 
 

@@ -5,6 +5,7 @@ Mirrors the reference CLI's subcommands on this path (pkg/src/vkt/cli.py):
     python -m paper_2203_10213_b200 filter --gaussian 1.0 --ksize 3 -i in.vkt -o out.vkt
     python -m paper_2203_10213_b200 filter --kernel-file k.txt [--mode wrap] < in.vkt > out.vkt
     python -m paper_2203_10213_b200 fill --value 0.5 [--roi X0 Y0 Z0 X1 Y1 Z1] -i in.vkt
+    python -m paper_2203_10213_b200 clahe --bricks 2 2 2 [--bins 256] [--clip 4] -i in.vkt
     python -m paper_2203_10213_b200 info -i in.vkt
     python -m paper_2203_10213_b200 raw-import --dims X Y Z --format u8 -i raw.bin
     python -m paper_2203_10213_b200 bench [--size 128] [--repeat 3]
@@ -75,6 +76,13 @@ def _build_parser() -> _Parser:
     p.add_argument("--mode", choices=["clamp", "wrap", "mirror", "border"], default="clamp",
                    help="address mode (the reference always clamps)")
     p.add_argument("--chunk-planes", type=int, default=0, help="z-planes per streamed chunk")
+
+    p = sub.add_parser("clahe", help="contrast limited adaptive histogram equalization")
+    _io_args(p)
+    p.add_argument("--bricks", type=int, nargs=3, required=True, metavar=("X", "Y", "Z"))
+    p.add_argument("--bins", type=int, default=256)
+    p.add_argument("--clip", type=float, default=math.inf,
+                   help="clip limit as a multiple of the uniform bin height (inf = off)")
 
     p = sub.add_parser("raw-import", help="wrap a headerless raw payload")
     _io_args(p)
@@ -188,6 +196,15 @@ def _cmd_filter(args) -> int:
     return 0
 
 
+def _cmd_clahe(args) -> int:
+    from .clahe import ClaheParams, clahe_equalize
+
+    volume = _read_volume_arg(args)
+    clahe_equalize(volume, ClaheParams(tuple(args.bricks), args.bins, args.clip))
+    _write_volume_out(args, volume)
+    return 0
+
+
 def _cmd_raw_import(args) -> int:
     if getattr(args, "input", None):
         try:
@@ -245,6 +262,7 @@ _COMMANDS = {
     "info": _cmd_info,
     "fill": _cmd_fill,
     "filter": _cmd_filter,
+    "clahe": _cmd_clahe,
     "raw-import": _cmd_raw_import,
     "bench": _cmd_bench,
 }

@@ -103,19 +103,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup(n_gpus: int):
+def dist_setup(n_gpus: int, test_single_gpu: bool = False):
+    """One process per GPU over NCCL.  ``test_single_gpu`` (testing only) runs
+    all ranks on cuda:0 over gloo with host-staged halo exchange, because
+    NCCL's spinning P2P kernels must not share one device."""
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if test_single_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if test_single_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -224,7 +230,7 @@ def run_ours(args):
     from paper_2203_10213_b200 import _capi
     from paper_2203_10213_b200.shard import ShardedVolume, apply_filter_sharded
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup(args.gpus, args.test_single_gpu)
     dev = torch.device("cuda", local)
     nx, ny, nz = WORKLOAD["dims"]
     fmt = vk.DataFormat.UINT16
@@ -238,6 +244,19 @@ def run_ours(args):
     del gen
     stream = torch.cuda.current_stream(dev)
     group = dist.group.WORLD if world > 1 else None
+    exchange = None
+    if args.test_single_gpu and world > 1:
+        from paper_2203_10213_b200.shard import exchange_halos_host_staged
+
+        exchange = lambda *a: exchange_halos_host_staged(*a, group=group)  # noqa: E731
+
+    red_dev = torch.device("cpu") if args.test_single_gpu else dev  # gloo reduces on the host
+
+    def allreduce(vals, op):
+        t = torch.tensor(vals, device=red_dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=op)
+        return [float(v) for v in t.cpu()]
 
     def barrier():
         if world > 1:
@@ -245,7 +264,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        apply_filter_sharded(dst, src, kernel, mode, group=group)
+        apply_filter_sharded(dst, src, kernel, mode, group=group, exchange=exchange)
     barrier()
 
     launches0 = _capi.launch_count()
@@ -255,16 +274,14 @@ def run_ours(args):
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            apply_filter_sharded(dst, src, kernel, mode, group=group, kernel_events=kev)
+            apply_filter_sharded(dst, src, kernel, mode, group=group, exchange=exchange,
+                                 kernel_events=kev)
         e1.record(stream)
         barrier()
     launches = _capi.launch_count() - launches0
     ms_total = e0.elapsed_time(e1)
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-    t = torch.tensor([ms_total, kern_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, kern_ms = float(t[0]), float(t[1])
+    ms_total, kern_ms = allreduce([ms_total, kern_ms], dist.ReduceOp.MAX)
     ms_step = ms_total / args.steps
     nvox = nx * ny * nz
     value = nvox / (ms_step / 1e3) / 1e9
@@ -299,20 +316,15 @@ def run_ours(args):
                              z_range=(src.z0 - lo, src.z1 - lo))
     f1.record(stream)
     barrier()
-    t2 = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t2[0]) / e2e_steps
+    e2e_ms = allreduce([f0.elapsed_time(f1)], dist.ReduceOp.MAX)[0] / e2e_steps
     e2e_value = nvox / (e2e_ms / 1e3) / 1e9
     # host result must equal the device-resident result
     e2e_ok = bool(torch.equal(pin_out[(src.z0 - lo) * plane_b:(src.z1 - lo) * plane_b],
                               dst.local.data.array.cpu()))
     h2d_bytes = (hi - lo) * plane_b
     d2h_bytes = (src.z1 - src.z0) * plane_b
-    hb = torch.tensor([h2d_bytes, d2h_bytes], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(hb)
-    h2d_total, d2h_total = int(hb[0]), int(hb[1])
+    h2d_total, d2h_total = (int(v) for v in allreduce([h2d_bytes, d2h_bytes], dist.ReduceOp.SUM))
+    e2e_ok = bool(allreduce([1.0 if e2e_ok else 0.0], dist.ReduceOp.MIN)[0] > 0.5)
     del np
 
     # ---- roofline of the dominant kernel (interior launch on each rank) ----
@@ -387,6 +399,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--test-single-gpu", action="store_true",
+                    help="testing only: all ranks on cuda:0 over gloo (numbers are not a benchmark)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: warm-up < 3 steps", file=sys.stderr)

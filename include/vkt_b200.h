@@ -161,6 +161,22 @@ int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t stream);
 /* dst = quantize(lo + (sum of the 8 blended brick mappings)*(hi - lo)). */
 int vkt_clahe_blend(const vkt_clahe_args* args, vkt_stream_t stream);
 
+/* ---- Resample / Flip ----
+ * Flip: reverse the stored cells along axis 0/1/2 (x/y/z) — a bit-exact
+ * permutation (pkg/src/vkt/ops/geometric.py:34-40).  src and dst must not
+ * alias. */
+int vkt_flip(const void* src, void* dst, vkt_int3 dims, int32_t format, int32_t axis,
+             vkt_stream_t stream);
+
+/* Resample a structured volume onto dst_dims cells (ops/core.py:202-262):
+ * destination cell centers map uniformly onto the source extent, trilinear
+ * samples of the mapped float64 grid with clamp-to-edge (volume.py:237-266),
+ * re-quantized into dst_format / dst mapping — float64 in numpy's operation
+ * order, bit-identical to the reference. */
+int vkt_resample(const void* src, vkt_int3 src_dims, int32_t src_format, double src_lo,
+                 double src_hi, void* dst, vkt_int3 dst_dims, int32_t dst_format, double dst_lo,
+                 double dst_hi, vkt_stream_t stream);
+
 /* Error class name for a status code (errors.py naming). */
 const char* vkt_status_name(int status);
 

@@ -173,6 +173,29 @@ def main():
         clahe[f"h{i:02d}/maps"] = maps
         clahe[f"h{i:02d}/spec"] = np.array([fmt, mapping[0], mapping[1], *bricks, bins, clip])
     np.savez_compressed(OUT / "clahe_cases.npz", **clahe)
+
+    # Resample / Flip (ops/core.py:202-262, ops/geometric.py:34-40)
+    xrng = np.random.default_rng(523)
+    xf = {}
+    rspecs = [((16, 12, 10), 1, (0.0, 1.0), (8, 6, 5), 1, (0.0, 1.0)),
+              ((13, 9, 7), 2, (-1.0, 3.0), (20, 4, 11), 3, (0.0, 1.0)),
+              ((10, 10, 10), 3, (0.0, 1.0), (7, 13, 3), 2, (-0.5, 1.5)),
+              ((1, 5, 3), 1, (0.0, 1.0), (4, 2, 6), 1, (0.0, 1.0)),
+              ((24, 24, 24), 3, (0.0, 1.0), (12, 12, 12), 3, (0.0, 1.0))]
+    for i, (dims, fmt, mapping, ddims, dfmt, dmap) in enumerate(rspecs):
+        stored = random_stored(xrng, dims, fmt)
+        v = vkt.StructuredVolume(dims, FMTS[fmt], (1, 0.5, 2), mapping)
+        v.array()[...] = stored
+        r = vkt.resample(v, ddims, FMTS[dfmt], dmap)
+        xf[f"r{i}/input"] = stored
+        xf[f"r{i}/output"] = r.array().copy()
+        xf[f"r{i}/spec"] = np.array([fmt, *mapping, *ddims, dfmt, *dmap])
+        xf[f"r{i}/cell"] = np.array(tuple(r.cell_size))
+        for ax in range(3):
+            f = v.copy()
+            vkt.flip(f, ax)
+            xf[f"r{i}/flip{ax}"] = f.array().copy()
+    np.savez_compressed(OUT / "transform_cases.npz", **xf)
     print(f"wrote {idx} filter cases, {len(specs)} fill cases, 3 VKTVOL01 files, {len(cspecs)} CLAHE cases to {OUT}")
 
 

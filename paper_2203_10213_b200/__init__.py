@@ -38,6 +38,7 @@ from .execution import (
 )
 from .clahe import ClaheParams, brick_mappings, clahe_equalize
 from .fill import Fill, FillRange, fill, fill_range
+from .transforms import flip, resample
 from .filters import (
     AddressMode,
     ApplyFilter,
@@ -86,4 +87,5 @@ __all__ = [
     "synthetic_host", "synthetic_structured", "timed", "with_policy",
     "filter_file", "load_raw", "read_range", "read_volume", "volume_from_bytes", "volume_to_bytes",
     "write_range", "write_volume", "ClaheParams", "brick_mappings", "clahe_equalize",
+    "flip", "resample",
 ]

@@ -36,6 +36,8 @@ EXPORTED_SYMBOLS = (
     "vkt_abi_version",
     "vkt_clahe_histograms",
     "vkt_clahe_blend",
+    "vkt_flip",
+    "vkt_resample",
 )
 
 

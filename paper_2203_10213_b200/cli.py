@@ -6,6 +6,8 @@ Mirrors the reference CLI's subcommands on this path (pkg/src/vkt/cli.py):
     python -m paper_2203_10213_b200 filter --kernel-file k.txt [--mode wrap] < in.vkt > out.vkt
     python -m paper_2203_10213_b200 fill --value 0.5 [--roi X0 Y0 Z0 X1 Y1 Z1] -i in.vkt
     python -m paper_2203_10213_b200 clahe --bricks 2 2 2 [--bins 256] [--clip 4] -i in.vkt
+    python -m paper_2203_10213_b200 resample --dims X Y Z [--format f32] [--range LO HI] -i in.vkt
+    python -m paper_2203_10213_b200 flip --axis y -i in.vkt
     python -m paper_2203_10213_b200 info -i in.vkt
     python -m paper_2203_10213_b200 raw-import --dims X Y Z --format u8 -i raw.bin
     python -m paper_2203_10213_b200 bench [--size 128] [--repeat 3]
@@ -83,6 +85,16 @@ def _build_parser() -> _Parser:
     p.add_argument("--bins", type=int, default=256)
     p.add_argument("--clip", type=float, default=math.inf,
                    help="clip limit as a multiple of the uniform bin height (inf = off)")
+
+    p = sub.add_parser("resample", help="resample onto a new structured grid")
+    _io_args(p)
+    p.add_argument("--dims", type=int, nargs=3, required=True, metavar=("X", "Y", "Z"))
+    p.add_argument("--format", choices=["u8", "u16", "f32"])
+    p.add_argument("--range", type=float, nargs=2, metavar=("LO", "HI"))
+
+    p = sub.add_parser("flip", help="mirror along an axis")
+    _io_args(p)
+    p.add_argument("--axis", choices=["x", "y", "z"], required=True)
 
     p = sub.add_parser("raw-import", help="wrap a headerless raw payload")
     _io_args(p)
@@ -205,6 +217,26 @@ def _cmd_clahe(args) -> int:
     return 0
 
 
+def _cmd_resample(args) -> int:
+    from .transforms import resample
+    from .volume import DataFormat, VoxelMapping
+
+    volume = _read_volume_arg(args)
+    fmt = DataFormat.parse(args.format) if args.format else None
+    mapping = VoxelMapping(*args.range) if args.range else None
+    _write_volume_out(args, resample(volume, args.dims, fmt, mapping))
+    return 0
+
+
+def _cmd_flip(args) -> int:
+    from .transforms import flip
+
+    volume = _read_volume_arg(args)
+    flip(volume, args.axis)
+    _write_volume_out(args, volume)
+    return 0
+
+
 def _cmd_raw_import(args) -> int:
     if getattr(args, "input", None):
         try:
@@ -263,6 +295,8 @@ _COMMANDS = {
     "fill": _cmd_fill,
     "filter": _cmd_filter,
     "clahe": _cmd_clahe,
+    "resample": _cmd_resample,
+    "flip": _cmd_flip,
     "raw-import": _cmd_raw_import,
     "bench": _cmd_bench,
 }

@@ -1,0 +1,182 @@
+// resample.cu — Flip and structured Resample.
+//
+// Flip (ops/geometric.py:34-40) is a permutation of stored cells: bit-exact.
+// Resample (ops/core.py:202-262 with sample_grid_linear, volume.py:237-266):
+// destination cell (i,j,k) samples the source at p = (i + 0.5) * src/dst
+// (source cell units), u = clamp(p - 0.5, 0, n - 1), i0 = min(floor(u),
+// max(n-2, 0)), f = u - i0, i1 = min(i0 + 1, n - 1), then the 7 lerps
+// a + t*(b - a) in the reference's order over the float64 mapped grid, and the
+// destination quantize (volume.py:102-110).  Every step is an IEEE float64
+// operation in numpy's order (no FMA contraction), so results are
+// bit-identical to the reference.
+#include "common.cuh"
+#include "dispatch.h"
+
+namespace vkt {
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) flip_kernel(const T* __restrict__ src, T* __restrict__ dst,
+                                                   int nx, int ny, int nz, int axis) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = i % nx, r = i / nx;
+    int64_t y = r % ny, z = r / ny;
+    if (axis == 0) x = nx - 1 - x;
+    else if (axis == 1) y = ny - 1 - y;
+    else z = nz - 1 - z;
+    dst[i] = src[(z * ny + y) * nx + x];
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ double mapped(T s, double lo, double span) {
+  if constexpr (FormatTraits<T>::is_int) {
+    return __dadd_rn(lo, __dmul_rn(__ddiv_rn((double)s, FormatTraits<T>::max_d), span));
+  } else {
+    return (double)s;
+  }
+}
+
+template <typename D>
+__device__ __forceinline__ D quantize_f64(double v, double lo, double span) {
+  if constexpr (FormatTraits<D>::is_int) {
+    double t = __ddiv_rn(__dsub_rn(v, lo), span);
+    t = fmin(fmax(t, 0.0), 1.0);
+    return (D)(uint32_t)floor(__dadd_rn(__dmul_rn(t, FormatTraits<D>::max_d), 0.5));
+  } else {
+    return __double2float_rn(v);
+  }
+}
+
+__device__ __forceinline__ double lerp(double a, double b, double t) {
+  return __dadd_rn(a, __dmul_rn(t, __dsub_rn(b, a)));
+}
+
+struct Axis {
+  int i0, i1;
+  double f;
+};
+
+__device__ __forceinline__ Axis axis_coord(int i, int n_src, double scale) {
+  // p = (i + 0.5) * scale ; u = p / 1.0 - 0.5 ; clip(u, 0, n - 1)
+  const double p = __dmul_rn(__dadd_rn((double)i, 0.5), scale);
+  double u = __dsub_rn(p, 0.5);
+  u = fmin(fmax(u, 0.0), (double)(n_src - 1));
+  int i0 = (int)floor(u);
+  const int cap = n_src - 2 > 0 ? n_src - 2 : 0;
+  if (i0 > cap) i0 = cap;
+  Axis a;
+  a.i0 = i0;
+  a.f = __dsub_rn(u, (double)i0);
+  a.i1 = i0 + 1 < n_src - 1 ? i0 + 1 : n_src - 1;
+  return a;
+}
+
+struct ResampleParams {
+  const void* src;
+  void* dst;
+  int sx, sy, sz, dx, dy, dz;
+  double slo, sspan, dlo, dspan;
+  double scale_x, scale_y, scale_z;
+};
+
+template <typename S, typename D>
+__global__ void __launch_bounds__(256) resample_kernel(ResampleParams p) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= p.dx) return;
+  const Axis ax = axis_coord(x, p.sx, p.scale_x);
+  const Axis ay = axis_coord(y, p.sy, p.scale_y);
+  const Axis az = axis_coord(z, p.sz, p.scale_z);
+  const S* g = static_cast<const S*>(p.src);
+  auto at = [&](int zz, int yy, int xx) {
+    return mapped<S>(g[((int64_t)zz * p.sy + yy) * p.sx + xx], p.slo, p.sspan);
+  };
+  const double c00 = lerp(at(az.i0, ay.i0, ax.i0), at(az.i0, ay.i0, ax.i1), ax.f);
+  const double c10 = lerp(at(az.i0, ay.i1, ax.i0), at(az.i0, ay.i1, ax.i1), ax.f);
+  const double c01 = lerp(at(az.i1, ay.i0, ax.i0), at(az.i1, ay.i0, ax.i1), ax.f);
+  const double c11 = lerp(at(az.i1, ay.i1, ax.i0), at(az.i1, ay.i1, ax.i1), ax.f);
+  const double c0 = lerp(c00, c10, ay.f);
+  const double c1 = lerp(c01, c11, ay.f);
+  const double v = lerp(c0, c1, az.f);
+  static_cast<D*>(p.dst)[((int64_t)z * p.dy + y) * p.dx + x] = quantize_f64<D>(v, p.dlo, p.dspan);
+}
+
+template <typename S>
+cudaError_t launch_resample_dst(const ResampleParams& p, int dst_format, cudaStream_t s) {
+  dim3 grid((p.dx + 255) / 256, p.dy, p.dz);
+  switch (dst_format) {
+    case VKT_U8: resample_kernel<S, uint8_t><<<grid, 256, 0, s>>>(p); break;
+    case VKT_U16: resample_kernel<S, uint16_t><<<grid, 256, 0, s>>>(p); break;
+    default: resample_kernel<S, float><<<grid, 256, 0, s>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+bool fmt_ok(int f) { return f == VKT_U8 || f == VKT_U16 || f == VKT_F32; }
+
+}  // namespace
+}  // namespace vkt
+
+using namespace vkt;
+
+extern "C" int vkt_flip(const void* src, void* dst, vkt_int3 dims, int32_t format, int32_t axis,
+                        vkt_stream_t stream) {
+  if (!src || !dst || src == dst || dims.x < 1 || dims.y < 1 || dims.z < 1 || !fmt_ok(format) ||
+      axis < 0 || axis > 2) {
+    set_error_detail("flip: invalid arguments (src/dst distinct, dims >= 1, axis 0..2)");
+    return VKT_INVALID_ARGUMENT;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = 148 * 8;
+  if (format == VKT_U8)
+    flip_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, dims.x, dims.y, dims.z, axis);
+  else if (format == VKT_U16)
+    flip_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, (uint16_t*)dst, dims.x, dims.y, dims.z, axis);
+  else
+    flip_kernel<float><<<grid, 256, 0, s>>>((const float*)src, (float*)dst, dims.x, dims.y, dims.z, axis);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error_detail("flip launch: %s", cudaGetErrorString(e));
+    return VKT_DEVICE_FAILURE;
+  }
+  return VKT_OK;
+}
+
+extern "C" int vkt_resample(const void* src, vkt_int3 src_dims, int32_t src_format, double src_lo,
+                            double src_hi, void* dst, vkt_int3 dst_dims, int32_t dst_format,
+                            double dst_lo, double dst_hi, vkt_stream_t stream) {
+  if (!src || !dst || src_dims.x < 1 || src_dims.y < 1 || src_dims.z < 1 || dst_dims.x < 1 ||
+      dst_dims.y < 1 || dst_dims.z < 1 || !fmt_ok(src_format) || !fmt_ok(dst_format) ||
+      !(src_lo < src_hi) || !(dst_lo < dst_hi) || dst_dims.y > 65535 || dst_dims.z > 65535) {
+    set_error_detail("resample: invalid arguments");
+    return VKT_INVALID_ARGUMENT;
+  }
+  ResampleParams p{};
+  p.src = src;
+  p.dst = dst;
+  p.sx = src_dims.x; p.sy = src_dims.y; p.sz = src_dims.z;
+  p.dx = dst_dims.x; p.dy = dst_dims.y; p.dz = dst_dims.z;
+  p.slo = src_lo; p.sspan = src_hi - src_lo;
+  p.dlo = dst_lo; p.dspan = dst_hi - dst_lo;
+  // scale = extent_cells / dst_dims in float64 (core.py:253)
+  p.scale_x = (double)src_dims.x / (double)dst_dims.x;
+  p.scale_y = (double)src_dims.y / (double)dst_dims.y;
+  p.scale_z = (double)src_dims.z / (double)dst_dims.z;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (src_format) {
+    case VKT_U8: e = launch_resample_dst<uint8_t>(p, dst_format, s); break;
+    case VKT_U16: e = launch_resample_dst<uint16_t>(p, dst_format, s); break;
+    default: e = launch_resample_dst<float>(p, dst_format, s); break;
+  }
+  count_launch();
+  if (e != cudaSuccess) {
+    set_error_detail("resample launch: %s", cudaGetErrorString(e));
+    return VKT_DEVICE_FAILURE;
+  }
+  return VKT_OK;
+}

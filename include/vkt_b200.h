@@ -70,7 +70,11 @@ enum {
    * (FP64 pipe); a parity/debug mode. */
   VKT_FLAG_EXACT_F64 = 1,
   /* Force the generic direct kernel even when the tiled TMA kernel applies. */
-  VKT_FLAG_FORCE_DIRECT = 2
+  VKT_FLAG_FORCE_DIRECT = 2,
+  /* vkt_apply_filter_host only: bound device memory to a few chunks (the
+   * input streams through ring buffers, halos copied device-to-device)
+   * instead of keeping the padded input resident when it fits. */
+  VKT_FLAG_HOST_BOUNDED = 4
 };
 
 /* Kernel paths reported by vkt_filter_path() */

@@ -21,6 +21,7 @@ U8, U16, F32 = 1, 2, 3
 WRAP, MIRROR, CLAMP, BORDER = 0, 1, 2, 3
 FLAG_EXACT_F64 = 1
 FLAG_FORCE_DIRECT = 2
+FLAG_HOST_BOUNDED = 4
 PATH_NONE, PATH_DIRECT, PATH_EXACT, PATH_TMA = 0, 1, 2, 3
 PATH_NAMES = {PATH_NONE: "none", PATH_DIRECT: "direct", PATH_EXACT: "exact", PATH_TMA: "tma"}
 

@@ -11,9 +11,15 @@
 //          bit-identical to a whole-volume launch,
 //   D2H  : downloads the chunk's output planes,
 // with the three phases of consecutive chunks overlapped on three streams
-// and NB buffer sets in rotation.  Only NB chunks are resident, so volumes
-// larger than HBM work.
+// and NB input and NB output buffers in rotation.  Only NB chunks are resident, so volumes
+// larger than HBM work.  Two details keep it at the PCIe floor: a chunk's
+// low halo (2*rz planes) is copied device-to-device from the previous
+// chunk's input instead of crossing PCIe again, and chunk sizes ramp up and
+// down at the ends (chunk_schedule) so the un-overlapped first upload and
+// last download are short.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "dispatch.h"
@@ -21,7 +27,7 @@
 namespace vkt {
 namespace {
 
-constexpr int NB = 3;  // buffer sets in flight
+constexpr int NB = 4;  // input buffers and output buffers in flight
 
 // Owns the pipeline's streams, events and device pool; on every exit path
 // (including errors) it drains the streams before releasing anything, so no
@@ -127,6 +133,31 @@ int upload_planes(uint8_t* dev, const HostSlab& h, int64_t g0, int count, int64_
   return VKT_OK;
 }
 
+// Chunk sizes for T output planes with at most C per chunk: a short ramp
+// (C/8, C/4, C/2) at both ends so the first upload and the last download —
+// the parts of the pipeline that overlap nothing — stay small, and equal
+// full-size chunks in between.
+std::vector<int> chunk_schedule(int T, int C) {
+  std::vector<int> ramp;
+  for (int d = 8; d >= 2; d /= 2)
+    if (C / d >= 4) ramp.push_back(C / d);
+  int rsum = 0;
+  for (int r : ramp) rsum += r;
+  std::vector<int> out;
+  if (T <= 2 * rsum + C) {  // short volume: equal chunks of at most C/2 (or C)
+    const int cmax = std::max(1, ramp.empty() ? C : ramp.back());
+    const int k = (T + cmax - 1) / cmax;
+    for (int i = 0; i < k; ++i) out.push_back(T / k + (i < T % k ? 1 : 0));
+    return out;
+  }
+  out = ramp;
+  const int mid = T - 2 * rsum;
+  const int k = (mid + C - 1) / C;
+  for (int i = 0; i < k; ++i) out.push_back(mid / k + (i < mid % k ? 1 : 0));
+  out.insert(out.end(), ramp.rbegin(), ramp.rend());
+  return out;
+}
+
 }  // namespace
 }  // namespace vkt
 
@@ -174,6 +205,8 @@ extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_
   int C = chunk_planes > 0 ? chunk_planes : (int)std::max<int64_t>(16, (128ll << 20) / plane_bytes);
   C = std::min(C, ze - zb);
 
+  const std::vector<int> sizes = chunk_schedule(ze - zb, C);
+
   HostCtx ctx;
   ctx.s_comp = s_comp;
   VKT_CK(cudaStreamCreateWithFlags(&ctx.s_h2d, cudaStreamNonBlocking), "stream");
@@ -185,37 +218,87 @@ extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_
   }
   VKT_CK(cudaEventCreateWithFlags(&ctx.alloc_done, cudaEventDisableTiming), "event");
 
-  // NB x ([rz | C | rz] input planes + C output planes), stream-ordered.
-  const int64_t in_bytes = (int64_t)(C + 2 * rz) * plane_bytes;
-  const int64_t out_bytes = (int64_t)C * plane_bytes;
-  const int64_t set_bytes = ((in_bytes + 255) / 256 + (out_bytes + 255) / 256) * 256;
-  VKT_CK(scratch_alloc(reinterpret_cast<void**>(&ctx.pool), NB * set_bytes, s_comp),
+  // Input: when the whole padded input [zb-rz, ze+rz) fits comfortably in
+  // free HBM it stays resident, each chunk uploads only its new planes and
+  // finds its halos already in place; otherwise NB ring buffers of
+  // [rz | C | rz] planes.  Output: NB ring buffers of C planes.
+  const int64_t total_in = (int64_t)(ze - zb + 2 * rz) * plane_bytes;
+  size_t free_b = 0, total_b = 0;
+  VKT_CK(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  const bool resident = !(a.flags & VKT_FLAG_HOST_BOUNDED) && total_in <= (int64_t)(free_b / 2);
+  const int64_t in_bytes = resident ? total_in : (int64_t)(C + 2 * rz) * plane_bytes;
+  const int64_t in_stride = (in_bytes + 255) / 256 * 256;
+  const int64_t out_stride = ((int64_t)C * plane_bytes + 255) / 256 * 256;
+  const int n_in = resident ? 1 : NB;
+  VKT_CK(scratch_alloc(reinterpret_cast<void**>(&ctx.pool), n_in * in_stride + NB * out_stride, s_comp),
          "scratch_alloc");
   uint8_t* pool = ctx.pool;
+  uint8_t* out_pool = pool + n_in * in_stride;
   VKT_CK(cudaEventRecord(ctx.alloc_done, s_comp), "event");
   VKT_CK(cudaStreamWaitEvent(ctx.s_h2d, ctx.alloc_done, 0), "wait");
   VKT_CK(cudaStreamWaitEvent(ctx.s_d2h, ctx.alloc_done, 0), "wait");
 
   const uint8_t* hsrc = static_cast<const uint8_t*>(a.src);
   uint8_t* hdst = static_cast<uint8_t*>(a.dst);
+  const HostSlab hs{hsrc, a.z_offset, nz, static_cast<const uint8_t*>(a.halo_lo),
+                    static_cast<const uint8_t*>(a.halo_hi), rz};
+  // VKT_HOST_TRACE=1: per-chunk stage timeline on stderr (diagnostics only)
+  const bool trace = std::getenv("VKT_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  mark(s_comp);
   int status = VKT_OK;
-  int c = 0;
-  for (int z0 = zb; z0 < ze && status == VKT_OK; z0 += C, ++c) {
-    const int z1 = std::min(z0 + C, ze);
-    const int n = z1 - z0;
+  int z0 = zb;
+  int uploaded_hi = zb - rz;  // resident input: planes below this are on the device
+  const uint8_t* prev_in = nullptr;  // previous chunk's input buffer (global planes [z0-n'-rz, z0+rz))
+  int prev_n = 0;
+  for (size_t c = 0; c < sizes.size() && status == VKT_OK; ++c) {
+    const int n = sizes[c];
+    const int z1 = z0 + n;
     const int b = c % NB;
-    uint8_t* in = pool + b * set_bytes;
-    uint8_t* out = in + (in_bytes + 255) / 256 * 256;
-    if (c >= NB) VKT_CK(cudaStreamWaitEvent(ctx.s_h2d, ctx.d2h_done[b], 0), "wait");
-    // [halo_lo | slab | halo_hi] = global planes [z0-rz, z1+rz) address-mapped
-    const HostSlab hs{hsrc, a.z_offset, nz, static_cast<const uint8_t*>(a.halo_lo),
-                      static_cast<const uint8_t*>(a.halo_hi), rz};
-    status = upload_planes(in, hs, a.z_offset + z0 - rz, n + 2 * rz, gnz, plane_bytes,
-                           a.address_mode, ctx.s_h2d);
+    uint8_t* out = out_pool + b * out_stride;
+    mark(ctx.s_h2d);
+    uint8_t* in;
+    if (resident) {
+      // global planes [z0-rz, z1+rz) sit at [z0-zb, z1-zb+2rz) of the buffer;
+      // everything below uploaded_hi is already there
+      in = pool + (int64_t)(z0 - zb) * plane_bytes;
+      const int from = std::max(z0 - rz, uploaded_hi);
+      status = upload_planes(pool + (int64_t)(from - (zb - rz)) * plane_bytes, hs, a.z_offset + from,
+                             z1 + rz - from, gnz, plane_bytes, a.address_mode, ctx.s_h2d);
+      uploaded_hi = z1 + rz;
+    } else {
+      in = pool + b * in_stride;
+      // input buffer b is free once chunk c-NB's filter has read it
+      if (c >= NB) VKT_CK(cudaStreamWaitEvent(ctx.s_h2d, ctx.comp_done[b], 0), "wait");
+      // [halo_lo | slab | halo_hi] = global planes [z0-rz, z1+rz) address-
+      // mapped.  The first 2*rz of them are the last 2*rz planes of the
+      // previous chunk's input: copy those device to device (same stream, so
+      // the previous upload has landed) and send only the new planes over PCIe.
+      int reuse = 0;
+      if (prev_in != nullptr && rz > 0) {
+        reuse = 2 * rz;
+        VKT_CK(cudaMemcpyAsync(in, prev_in + (int64_t)prev_n * plane_bytes, (int64_t)reuse * plane_bytes,
+                               cudaMemcpyDeviceToDevice, ctx.s_h2d),
+               "D2D halo");
+      }
+      status = upload_planes(in + (int64_t)reuse * plane_bytes, hs, a.z_offset + z0 - rz + reuse,
+                             n + 2 * rz - reuse, gnz, plane_bytes, a.address_mode, ctx.s_h2d);
+    }
     if (status != VKT_OK) break;
     VKT_CK(cudaEventRecord(ctx.h2d_done[b], ctx.s_h2d), "event");
+    mark(ctx.s_h2d);
 
     VKT_CK(cudaStreamWaitEvent(s_comp, ctx.h2d_done[b], 0), "wait");
+    // output buffer b is free once chunk c-NB's download has drained it
+    if (c >= NB) VKT_CK(cudaStreamWaitEvent(s_comp, ctx.d2h_done[b], 0), "wait");
+    mark(s_comp);
     vkt_filter_args ca = a;
     ca.src = in + (int64_t)rz * plane_bytes;
     ca.dst = out;
@@ -229,17 +312,36 @@ extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_
     status = vkt_apply_filter(&ca, reinterpret_cast<vkt_stream_t>(s_comp));
     if (status != VKT_OK) break;
     VKT_CK(cudaEventRecord(ctx.comp_done[b], s_comp), "event");
+    mark(s_comp);
 
     VKT_CK(cudaStreamWaitEvent(ctx.s_d2h, ctx.comp_done[b], 0), "wait");
+    mark(ctx.s_d2h);
     VKT_CK(cudaMemcpyAsync(hdst + (int64_t)z0 * plane_bytes, out, (int64_t)n * plane_bytes,
                            cudaMemcpyDeviceToHost, ctx.s_d2h),
            "D2H chunk");
     VKT_CK(cudaEventRecord(ctx.d2h_done[b], ctx.s_d2h), "event");
+    mark(ctx.s_d2h);
+    prev_in = in;
+    prev_n = n;
+    z0 = z1;
   }
   // drain (the pool is released by ~HostCtx after the last download)
   cudaError_t e1 = cudaStreamSynchronize(ctx.s_h2d);
   cudaError_t e2 = cudaStreamSynchronize(ctx.s_d2h);
   cudaError_t e3 = cudaStreamSynchronize(s_comp);
+  if (trace) {
+    auto t = [&](size_t i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      return ms;
+    };
+    for (size_t c = 0; 1 + 6 * c + 5 < tev.size(); ++c) {
+      const size_t i = 1 + 6 * c;
+      std::fprintf(stderr, "chunk %2zu n=%3d  h2d %7.2f-%7.2f  filter %7.2f-%7.2f  d2h %7.2f-%7.2f\n", c,
+                   sizes[c], t(i), t(i + 1), t(i + 2), t(i + 3), t(i + 4), t(i + 5));
+    }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
   if (status != VKT_OK) return status;
   for (cudaError_t e : {e1, e2, e3})
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline");

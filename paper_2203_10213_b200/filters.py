@@ -235,7 +235,8 @@ def apply_filter(volume: StructuredVolume, kernel: Kernel, address_mode=AddressM
 
 def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *, fmt=None,
                       mapping=(0.0, 1.0), out=None, z_range=None, chunk_planes: int = 0,
-                      z_offset: int = 0, global_nz: int = 0, halo_lo=None, halo_hi=None):
+                      z_offset: int = 0, global_nz: int = 0, halo_lo=None, halo_hi=None,
+                      bounded_memory: bool = False):
     """ApplyFilter on a HOST (z, y, x) array, streamed through HBM.
 
     The reference filters host numpy arrays (filters.py:69-95); this keeps that
@@ -253,6 +254,10 @@ def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *,
     outputs need must be inside it, unless ``halo_lo`` / ``halo_hi`` (host
     arrays of rz = kz//2 planes: the address-mapped planes just below and
     above the array) supply them.  ``z_range`` is relative to the array.
+
+    The padded input is kept resident on the device when it fits in half the
+    free HBM (each chunk uploads only its new planes); ``bounded_memory``
+    streams it through a few chunk-sized ring buffers instead.
     """
     import torch
 
@@ -289,7 +294,8 @@ def apply_filter_host(stored, kernel: Kernel, address_mode=AddressMode.CLAMP, *,
         halos.append(h.ctypes.data)
     args, _keep = make_args(out.ctypes.data, src.ctypes.data, (nx, ny, nz), fmt, mapping, kernel, mode,
                             out_z_begin=zb, out_z_end=ze, z_offset=z_offset, global_nz=global_nz,
-                            halo_lo=halos[0], halo_hi=halos[1], flags=_flags(get_execution_policy()))
+                            halo_lo=halos[0], halo_hi=halos[1],
+                            flags=_flags(get_execution_policy()) | (_capi.FLAG_HOST_BOUNDED if bounded_memory else 0))
     stream = int(torch.cuda.current_stream().cuda_stream) if torch.cuda.is_available() else 0
     _capi.check(_capi.load().vkt_apply_filter_host(ctypes.byref(args), int(chunk_planes),
                                                    ctypes.c_void_p(stream)))

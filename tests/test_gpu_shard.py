@@ -164,6 +164,8 @@ def test_host_api_bit_identical_to_device(mode, fmt, k, chunk):
     want = _unsharded(host, fmt, kern, mode)
     got = vk.apply_filter_host(host, kern, mode, chunk_planes=chunk)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+    got = vk.apply_filter_host(host, kern, mode, chunk_planes=chunk, bounded_memory=True)
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
     # a z sub-range writes only those planes
     out = np.zeros_like(host)
     vk.apply_filter_host(host, kern, mode, out=out, z_range=(4, 17), chunk_planes=chunk)
@@ -211,3 +213,23 @@ def test_host_api_slab_buffers_match_whole_volume():
     with pytest.raises(vk.InvalidArgument):
         vk.apply_filter_host(np.ascontiguousarray(host[0:16]), kern, "wrap", z_offset=0, global_nz=40,
                              z_range=(0, 13))
+
+
+@pytest.mark.parametrize("bounded", [False, True])
+@pytest.mark.parametrize("mode", list(vk.AddressMode))
+@pytest.mark.parametrize("kd,chunk", [((7, 7, 7), 16), ((9, 9, 9), 16), ((3, 3, 3), 40), ((5, 5, 5), 0)])
+def test_host_api_ramped_chunks_and_halo_reuse(mode, kd, chunk, bounded):
+    """Ramped chunk schedule (C/4, C/2, C.., C/2, C/4) with the low halo of each
+    chunk copied device-to-device from the previous chunk's input: chunks
+    smaller than the 2*rz halo included (9^3 kernel, 4-plane ramp chunks)."""
+    rng = np.random.default_rng(sum(kd) + chunk)
+    host = rng.integers(0, 65536, size=(70, 18, 64), dtype=np.uint16)
+    w = rng.random(kd[0] * kd[1] * kd[2])
+    kern = vk.Kernel(kd, w / w.sum())
+    want = _unsharded(host, vk.DataFormat.UINT16, kern, mode)
+    got = vk.apply_filter_host(host, kern, mode, chunk_planes=chunk, bounded_memory=bounded)
+    assert np.array_equal(got, want)
+    out = np.zeros_like(host)
+    vk.apply_filter_host(host, kern, mode, out=out, z_range=(9, 61), chunk_planes=chunk,
+                         bounded_memory=bounded)
+    assert np.array_equal(out[9:61], want[9:61])

@@ -27,7 +27,7 @@ pin.copy_(src.data.array)
 hin = pin.numpy().view(np.uint16).reshape(n, n, n)
 hout = pin2.numpy().view(np.uint16).reshape(n, n, n)
 k = vk.gaussian_kernel(1.5)
-for chunk in (32, 64, 128, 256, 512):
+for chunk in (16, 32, 64, 128, 256):
     vk.apply_filter_host(hin, k, out=hout, chunk_planes=chunk)
     t = time.perf_counter()
     for _ in range(3):

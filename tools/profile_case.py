@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--fmt", default="u16")
     ap.add_argument("--k", type=int, default=7)
     ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--nz", type=int, default=0, help="z extent (default n)")
     ap.add_argument("--mode", default="clamp")
     ap.add_argument("--kernel", default="gauss", choices=["gauss", "box", "lap"])
     ap.add_argument("--reps", type=int, default=3)
@@ -28,7 +29,7 @@ def main():
     fmt = vk.DataFormat.parse(args.fmt)
     k = {"gauss": lambda: vk.gaussian_kernel(1.0 if args.k < 7 else 1.5, args.k),
          "box": lambda: vk.box_kernel(args.k), "lap": vk.laplacian_kernel}[args.kernel]()
-    dims = (args.n, args.n, args.n)
+    dims = (args.n, args.n, args.nz or args.n)
     src = vk.synthetic_device(dims, fmt, seed=7)
     dst = vk.StructuredVolume(src.dims, fmt, data=vk.DeviceBuffer(src.nbytes, zero=False))
     vk.set_execution_policy(vk.ExecutionPolicy(filter_path=args.path))
@@ -41,9 +42,9 @@ def main():
         e1.record(s)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-    nvox = args.n ** 3
+    nvox = dims[0] * dims[1] * dims[2]
     best = min(times)
-    print(f"{args.fmt} k={args.k} {args.kernel} n={args.n} {args.mode} path={vk.filter_path(dst, src, k, args.mode)}: "
+    print(f"{args.fmt} k={args.k} {args.kernel} dims={dims} {args.mode} path={vk.filter_path(dst, src, k, args.mode)}: "
           f"best {best:.3f} ms = {nvox / best / 1e6:.1f} GVox/s  (all: {[round(t, 3) for t in times]})")
 
 

@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cstdlib>
 // filter_tma.cu — host side of the tiled TMA ApplyFilter kernel: eligibility,
 // tensor-map encoding (driver entry point, no libcuda link), chunk sizing and
 // dispatch.  The kernels are instantiated per voxel format in
@@ -131,6 +133,7 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
       zc = z;
     }
   }
+  if (const char* e = std::getenv("VKT_TMA_ZC")) zc = std::max(1, std::min(nzo, std::atoi(e)));  // diagnostics
   p.zc = zc;
   dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + tma::TY - 1) / tma::TY,
             (nzo + zc - 1) / zc);

@@ -107,12 +107,17 @@ struct Cfg {
   static_assert(BX <= 256 && BY <= 256, "TMA box too large");
 };
 
-// Weights as a kernel-parameter block, each (dz, dy) row of K taps padded to a
-// 16-byte boundary so a row is fetched with 128-bit uniform constant loads.
+// Weights as a kernel-parameter block laid out for the paired accumulators
+// (see plane_step): for each dy, NP = K/2 rows of K float2 pairs
+// (w[dz_a][dy][dx], w[dz_b][dy][dx]) for accumulator slots (2p, 2p+1)
+// (dz_a = K-1-2p, dz_b = K-2-2p), then the dz = 0 row for the unpaired slot
+// K-1, padded to 16 bytes.  Each pair is one 64-bit uniform constant load.
 template <int K>
 struct alignas(16) Weights {
+  static constexpr int NP = K / 2;
   static constexpr int KP = (K + 3) / 4 * 4;
-  float w[K * K * KP];
+  float2 wp[K * NP * K];
+  float ws[K * KP];
 };
 
 struct TmaParams {
@@ -435,44 +440,112 @@ __device__ __forceinline__ void store8<uint8_t>(uint8_t* out, const float (&a)[X
                                                    q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24)));
 }
 
+// Packed fp32x2 helpers (sm_100 FFMA2).  Each lane is an IEEE fma.rn.f32,
+// so a paired update is bit-identical to two FFMAs.
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2lo(uint64_t v) {
+  float lo;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float f2hi(uint64_t v) {
+  float hi;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(v));
+  return hi;
+}
+// (c.lo + x * w.lo, c.hi + x * w.hi): x is broadcast (SASS: FFMA2 R.F32,
+// UR.F32x2, R.F32x2), the weight pair sits in a uniform register pair.
+__device__ __forceinline__ uint64_t ffma2_bx(float x, uint64_t w, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pack(x, x)), "l"(w), "l"(c));
+  return r;
+}
+
+// Rolling accumulators of one thread: slot m holds the partial sums of the
+// output plane the current input plane reaches with dz = K-1-m.  Slots
+// (2p, 2p+1) live as packed pairs so one FFMA2 advances two output planes
+// (same input value, the weights of their two dz); slot K-1 is single.
+template <int K>
+struct Accum {
+  static constexpr int YPT = Layout<K>::YPT;
+  static constexpr int NP = K / 2;
+  uint64_t p[YPT][NP][XPT];
+  float s[YPT][XPT];
+};
+
 // One input plane's contribution to the K rolling accumulators of the
-// thread's 2 x 8 outputs (rows 2*ty and 2*ty+1).  GUARD: skip slots whose
-// output plane is outside the chunk (ramp up / down).
-template <int K, bool GUARD>
+// thread's YPT x 8 outputs.  GUARD: skip slot groups whose output planes are
+// all outside the chunk (ramp up / down; those sums are never stored).
+// PF: load the rows of dy+1 while dy computes (measured: +3% for f32 K>=5;
+// for the integer kernels the extra 16 registers push the weights off the
+// uniform datapath, -10%).
+template <int K, bool GUARD, bool PF>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage, int tx, int ty,
-                                           const Weights<K>& wt,
-                                           float (&acc)[Layout<K>::YPT][K][XPT], int first,
+                                           const Weights<K>& wt, Accum<K>& acc, int first,
                                            int last) {
   constexpr int YPT = Layout<K>::YPT;
   constexpr int R = K / 2;
+  constexpr int NP = K / 2;
   constexpr int OFF = 4 - R;
+  float4 nx[YPT][4];
+  const float* base = stage + YPT * ty * RP + XPT * tx;
+  if (PF) {
+#pragma unroll
+    for (int r = 0; r < YPT; ++r)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) nx[r][i] = reinterpret_cast<const float4*>(base + r * RP)[i];
+  }
 #pragma unroll(K <= 3 ? K : 1)
   for (int dy = 0; dy < K; ++dy) {
+    if (!PF) {
+#pragma unroll
+      for (int r = 0; r < YPT; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) nx[r][i] = reinterpret_cast<const float4*>(base + (r + dy) * RP)[i];
+    }
     float v[YPT][16];
 #pragma unroll
     for (int r = 0; r < YPT; ++r) {
-      const float4* row = reinterpret_cast<const float4*>(stage + (YPT * ty + r + dy) * RP + XPT * tx);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float4 q = row[i];
-        v[r][4 * i + 0] = q.x;
-        v[r][4 * i + 1] = q.y;
-        v[r][4 * i + 2] = q.z;
-        v[r][4 * i + 3] = q.w;
+        v[r][4 * i + 0] = nx[r][i].x;
+        v[r][4 * i + 1] = nx[r][i].y;
+        v[r][4 * i + 2] = nx[r][i].z;
+        v[r][4 * i + 3] = nx[r][i].w;
       }
     }
+    if (PF && dy + 1 < K) {
 #pragma unroll
-    for (int m = 0; m < K; ++m) {
-      if (GUARD && (m < first || m > last)) continue;
-      const int dz = K - 1 - m;
-      const float* w = wt.w + (dz * K + dy) * Weights<K>::KP;
+      for (int r = 0; r < YPT; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) nx[r][i] = reinterpret_cast<const float4*>(base + (r + dy + 1) * RP)[i];
+    }
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      if (GUARD && (2 * pp + 1 < first || 2 * pp > last)) continue;
+      const uint64_t* w = reinterpret_cast<const uint64_t*>(wt.wp + (dy * NP + pp) * K);
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx) {
+        const uint64_t wv = w[dx];
+#pragma unroll
+        for (int r = 0; r < YPT; ++r)
+#pragma unroll
+          for (int j = 0; j < XPT; ++j) acc.p[r][pp][j] = ffma2_bx(v[r][OFF + j + dx], wv, acc.p[r][pp][j]);
+      }
+    }
+    if (!GUARD || (K - 1 >= first && K - 1 <= last)) {
+      const float* w = wt.ws + dy * Weights<K>::KP;
 #pragma unroll
       for (int dx = 0; dx < K; ++dx) {
         const float wv = w[dx];
 #pragma unroll
         for (int r = 0; r < YPT; ++r)
 #pragma unroll
-          for (int j = 0; j < XPT; ++j) acc[r][m][j] = __fmaf_rn(wv, v[r][OFF + j + dx], acc[r][m][j]);
+          for (int j = 0; j < XPT; ++j) acc.s[r][j] = __fmaf_rn(wv, v[r][OFF + j + dx], acc.s[r][j]);
       }
     }
   }
@@ -576,13 +649,17 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
   const int tx = tid % (TX / XPT);
   const int ty = tid / (TX / XPT);
   const float a0 = acc_init<T>(p.c);
-  float acc[YPT][K][XPT];
+  constexpr int NP = K / 2;
+  const uint64_t a00 = f2pack(a0, a0);
+  Accum<K> acc;
 #pragma unroll
   for (int r = 0; r < YPT; ++r)
 #pragma unroll
-    for (int m = 0; m < K; ++m)
+    for (int j = 0; j < XPT; ++j) {
 #pragma unroll
-      for (int j = 0; j < XPT; ++j) acc[r][m][j] = a0;
+      for (int pp = 0; pp < NP; ++pp) acc.p[r][pp][j] = a00;
+      acc.s[r][j] = a0;
+    }
 
   const int ox = x0 + tx * XPT;
   const int oy = y0 + YPT * ty;
@@ -633,28 +710,33 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
     if (first <= 0 && last >= K - 1)
-      plane_step<K, false>(stage, tx, ty, wt, acc, 0, K - 1);
+      plane_step<K, false, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, 0, K - 1);
     else
-      plane_step<K, true>(stage, tx, ty, wt, acc, first, last);
+      plane_step<K, true, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, first, last);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
     if (i >= 2 * R) {
       const int oz = zo0 + i - 2 * R;
 #pragma unroll
-      for (int r = 0; r < YPT; ++r)
-        if (valid[r] > 0)
-          store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.pitch, acc[r][0], valid[r]);
+      for (int r = 0; r < YPT; ++r) {
+        float o[XPT];
+#pragma unroll
+        for (int j = 0; j < XPT; ++j) o[j] = f2lo(acc.p[r][0][j]);
+        if (valid[r] > 0) store8<T>(out_base + (int64_t)oz * plane_elems + (int64_t)r * p.pitch, o, valid[r]);
+      }
     }
+    // roll: slot m <- slot m+1, slot K-1 <- fresh
 #pragma unroll
-    for (int r = 0; r < YPT; ++r) {
+    for (int r = 0; r < YPT; ++r)
 #pragma unroll
-      for (int m = 0; m < K - 1; ++m)
+      for (int j = 0; j < XPT; ++j) {
 #pragma unroll
-        for (int j = 0; j < XPT; ++j) acc[r][m][j] = acc[r][m + 1][j];
-#pragma unroll
-      for (int j = 0; j < XPT; ++j) acc[r][K - 1][j] = a0;
-    }
+        for (int pp = 0; pp + 1 < NP; ++pp)
+          acc.p[r][pp][j] = f2pack(f2hi(acc.p[r][pp][j]), f2lo(acc.p[r][pp + 1][j]));
+        acc.p[r][NP - 1][j] = f2pack(f2hi(acc.p[r][NP - 1][j]), acc.s[r][j]);
+        acc.s[r][j] = a0;
+      }
   }
 }
 
@@ -662,9 +744,16 @@ template <typename T, int K, int MODE>
 cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, const CUtensorMap& mh,
                               const TmaParams& p, const float* w32, dim3 grid, cudaStream_t s) {
   using C = Cfg<T, K>;
+  // w32: (dz, dy, dx), x fastest
   Weights<K> wt = {};
-  for (int r = 0; r < K * K; ++r)
-    for (int x = 0; x < K; ++x) wt.w[r * Weights<K>::KP + x] = w32[r * K + x];
+  constexpr int NP = Weights<K>::NP;
+  for (int dy = 0; dy < K; ++dy) {
+    for (int pp = 0; pp < NP; ++pp)
+      for (int dx = 0; dx < K; ++dx)
+        wt.wp[(dy * NP + pp) * K + dx] = make_float2(w32[((K - 1 - 2 * pp) * K + dy) * K + dx],
+                                                     w32[((K - 2 - 2 * pp) * K + dy) * K + dx]);
+    for (int dx = 0; dx < K; ++dx) wt.ws[dy * Weights<K>::KP + dx] = w32[dy * K + dx];
+  }
   auto fn = filter_tma_kernel<T, K, MODE>;
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (err != cudaSuccess) return err;

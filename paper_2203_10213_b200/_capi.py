@@ -9,12 +9,14 @@ is missing, every device call raises ``DeviceFailure``.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import DeviceFailure, from_status_name
 
-LIB_PATH = Path(__file__).resolve().parent / "libvkt_b200.so"
+# VKT_LIB: load a diagnostics build (build.py --variant=...) instead
+LIB_PATH = Path(os.environ.get("VKT_LIB") or Path(__file__).resolve().parent / "libvkt_b200.so")
 
 # enums (vkt_b200.h)
 U8, U16, F32 = 1, 2, 3

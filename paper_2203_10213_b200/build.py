@@ -49,8 +49,15 @@ def _headers_mtime() -> float:
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False,
+          defines: tuple[str, ...] = (), variant: str = "") -> Path:
+    """Build libvkt_b200.so.  ``variant``/``defines``: a diagnostics build
+    (e.g. -DVKT_EXP_NOCONVERT) into build/<variant>/libvkt_b200.so, loaded
+    with VKT_LIB=<path>; never the product library."""
     nvcc = _nvcc()
+    BUILD = ROOT / "build" / ("obj" if not variant else f"obj_{variant}")
+    LIB = PKG / "libvkt_b200.so" if not variant else ROOT / "build" / variant / "libvkt_b200.so"
+    LIB.parent.mkdir(parents=True, exist_ok=True)
     BUILD.mkdir(parents=True, exist_ok=True)
     hdr_t = _headers_mtime()
     objs = []
@@ -59,7 +66,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         obj = BUILD / (src.stem + ".o")
         objs.append(obj)
         if force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, hdr_t):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *defines, "-c", str(src), "-o", str(obj)]
             if ptxas_verbose:
                 cmd[1:1] = ["-Xptxas", "-v"]
             jobs.append((src, cmd))
@@ -93,5 +100,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
 
 if __name__ == "__main__":
     args = set(sys.argv[1:])
-    p = build(verbose="-v" in args, force="-f" in args, ptxas_verbose="--ptxas" in args)
+    variant = next((a.split("=", 1)[1] for a in args if a.startswith("--variant=")), "")
+    p = build(verbose="-v" in args, force="-f" in args, ptxas_verbose="--ptxas" in args,
+              defines=tuple(sorted(a for a in args if a.startswith("-D"))), variant=variant)
     print(p)

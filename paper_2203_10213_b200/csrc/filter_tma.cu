@@ -25,10 +25,10 @@ extern template cudaError_t launch_tma_dtype<uint16_t>(int, int, const CUtensorM
                                                        const CUtensorMap&, const CUtensorMap&,
                                                        const TmaParams&, const float*, dim3,
                                                        cudaStream_t);
-extern template cudaError_t launch_tma_dtype<float>(int, int, const CUtensorMap&,
-                                                    const CUtensorMap&, const CUtensorMap&,
-                                                    const TmaParams&, const float*, dim3,
-                                                    cudaStream_t);
+template <>  // explicit specialization (filter_tma_f32.cu): K <= 5 -> filter_tma_zp.cuh
+cudaError_t launch_tma_dtype<float>(int, int, const CUtensorMap&, const CUtensorMap&,
+                                    const CUtensorMap&, const TmaParams&, const float*, dim3,
+                                    cudaStream_t);
 }  // namespace tma
 
 namespace {
@@ -120,7 +120,9 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   // estimated time  waves(ZC) * (ZC + 2R + fill)  (fill ~ 3 planes).
   const int nzo = plan.z_end - plan.z_begin;
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
-  const int64_t slots = 148ll * (k == 7 ? tma::Layout<7>::CTAS_PER_SM : tma::Layout<3>::CTAS_PER_SM);
+  // CTAs per SM: 2 for K = 7, 3 for K <= 5 (u8/u16 paired kernel and the
+  // f32 filter_tma_zp.cuh variant alike)
+  const int64_t slots = 148ll * (k == 7 ? tma::Layout<2, 7>::CTAS_PER_SM : tma::Layout<2, 3>::CTAS_PER_SM);
   int zc = 64;
   double best = 1e300;
   for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {

@@ -213,11 +213,12 @@ __device__ __forceinline__ void ffma2_bw(uint64_t x, float w, uint64_t& c) {
   // rolled dy loop instead of being renamed with moves at the back edge
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(x), "l"(f2pack(w, w)));
 }
-// Two u8/u16 values -> (float, float) exactly: the value v in the low
-// mantissa bits of 2^23 (bits 0x4B000000 | v) minus 2^23, one FADD2.
-__device__ __forceinline__ uint64_t widen2(uint32_t vlo, uint32_t vhi) {
-  const uint64_t bits = (uint64_t)(0x4B000000u | vlo) | ((uint64_t)(0x4B000000u | vhi) << 32);
-  uint64_t r;
+// Two u8/u16 values, given as the bit patterns 0x4B000000 | v (the value in
+// the low mantissa bits of 2^23), -> (float, float) exactly: minus 2^23, one
+// FADD2.
+__device__ __forceinline__ uint64_t widen2(uint32_t blo, uint32_t bhi) {
+  uint64_t bits, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bits) : "r"(blo), "r"(bhi));
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(bits), "l"(f2pack(-8388608.0f, -8388608.0f)));
   return r;
 }
@@ -264,8 +265,7 @@ struct StagePlan {
   static constexpr int GPR = NPR / 4;  // items per row
   static constexpr int NQ = GPR * C::BY;
   static constexpr int QPT = (NQ + NT - 1) / NT;
-  // K = 7 runs at the 128-register budget: recompute instead of storing.
-  static constexpr bool STORE = K <= 5;
+  static constexpr bool STORE = true;  // offsets computed once per CTA
   int rdy_[STORE ? QPT : 1];  // ready-stage float offset (-1: no item)
   uint32_t slow_;             // bit k: item k takes the per-cell edge path
   int t_, rows_lo_, rows_hi_, e_lo_, e_hi_;
@@ -308,22 +308,23 @@ struct StagePlan {
   }
 };
 
-// 4 consecutive raw cells -> 4 floats (u8/u16 as exponent-trick bit patterns
-// to be finished by widen2, f32 as values).
+// 4 consecutive raw cells -> 4 words: u8/u16 as the exponent-trick bit
+// patterns 0x4B000000 | v (one PRMT each; widen2 finishes them), f32 as
+// the values' bits.
 template <typename T>
 __device__ __forceinline__ void load_quad(const T* src, uint32_t (&b)[4]) {
   if constexpr (sizeof(T) == 2) {
     const uint2 w = *reinterpret_cast<const uint2*>(src);
-    b[0] = w.x & 0xFFFFu;
-    b[1] = w.x >> 16;
-    b[2] = w.y & 0xFFFFu;
-    b[3] = w.y >> 16;
+    b[0] = __byte_perm(w.x, 0x4B000000u, 0x7410);
+    b[1] = __byte_perm(w.x, 0x4B000000u, 0x7432);
+    b[2] = __byte_perm(w.y, 0x4B000000u, 0x7410);
+    b[3] = __byte_perm(w.y, 0x4B000000u, 0x7432);
   } else if constexpr (sizeof(T) == 1) {
     const uint32_t w = *reinterpret_cast<const uint32_t*>(src);
-    b[0] = w & 0xFFu;
-    b[1] = (w >> 8) & 0xFFu;
-    b[2] = (w >> 16) & 0xFFu;
-    b[3] = w >> 24;
+    b[0] = __byte_perm(w, 0x4B000000u, 0x7440);
+    b[1] = __byte_perm(w, 0x4B000000u, 0x7441);
+    b[2] = __byte_perm(w, 0x4B000000u, 0x7442);
+    b[3] = __byte_perm(w, 0x4B000000u, 0x7443);
   } else {
     const uint4 w = *reinterpret_cast<const uint4*>(src);
     b[0] = w.x;
@@ -594,7 +595,9 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
       issue(i - 1 + SR);
     }
     if (i + C::AHEAD < np) prepare(i + C::AHEAD);
+#ifndef VKT_EXP_NOREADYWAIT
     mbar_wait(&ready[s], (uint32_t)((i / S) & 1));
+#endif
 #endif
     // slot m <-> output plane zo0 + i - 2R + m
     const int first = 2 * R - i;

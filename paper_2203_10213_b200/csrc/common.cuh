@@ -39,6 +39,21 @@ __host__ __device__ __forceinline__ int64_t map_index(int64_t i, int64_t n) {
   }
 }
 
+// Single-fold variant, exact when -n <= i < 2n (a halo overshooting the
+// volume by at most n cells): no integer division.
+template <int MODE>
+__host__ __device__ __forceinline__ int map_index_near(int i, int n) {
+  if constexpr (MODE == VKT_CLAMP) {
+    return i < 0 ? 0 : (i >= n ? n - 1 : i);
+  } else if constexpr (MODE == VKT_WRAP) {
+    return i < 0 ? i + n : (i >= n ? i - n : i);
+  } else if constexpr (MODE == VKT_MIRROR) {
+    return i < 0 ? -1 - i : (i >= n ? 2 * n - 1 - i : i);
+  } else {
+    return (i >= 0 && i < n) ? i : -1;
+  }
+}
+
 // 32-bit variant for the x/y axes (extents < 2^31).
 template <int MODE>
 __host__ __device__ __forceinline__ int map_index32(int i, int n) {

@@ -366,8 +366,10 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
       for (int c = 0; c < 8; ++c) {
         const int gx = x0 - 4 + e + (c & 3) + (c >> 2) * HALF;
         if ((yo || gx < 0 || gx >= p.nx) && gx >= x0 - R && gx < x0 + TX + R) {
-          const int mx = map_index32<MODE>(gx, p.nx);
-          const int my = map_index32<MODE>(gy, p.ny);
+          // halo cells overshoot by <= R <= 4: one fold is exact for extents >= 4
+          const bool near = p.nx >= 4 && p.ny >= 4;
+          const int mx = near ? map_index_near<MODE>(gx, p.nx) : map_index32<MODE>(gx, p.nx);
+          const int my = near ? map_index_near<MODE>(gy, p.ny) : map_index32<MODE>(gy, p.ny);
           float v;
           if constexpr (MODE == VKT_WRAP)
             v = widen(__ldg(plane + (int64_t)my * p.pitch + mx));

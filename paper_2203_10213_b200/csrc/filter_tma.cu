@@ -81,6 +81,7 @@ bool tma_supported(const vkt_filter_args& a) {
   const int k = a.kdims.x;
   if (a.kdims.y != k || a.kdims.z != k) return false;
   if (k != 3 && k != 5 && k != 7) return false;
+
   // rows that are not 16-byte multiples (or unaligned buffers) are staged
   // through pitched scratch copies (launch_filter_tma), so every extent works
   return encode_fn() != nullptr;

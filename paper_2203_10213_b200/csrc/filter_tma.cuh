@@ -34,6 +34,8 @@
 
 #include <cuda.h>
 
+#include <cstdio>
+
 #include "common.cuh"
 
 namespace vkt {
@@ -91,7 +93,15 @@ struct Cfg {
   // the fastest and the slowest warp) once 6 raw TMA stages fit (TMA
   // lookahead S_RAW - 1 - AHEAD planes: f32 K <= 5 planes take ~2 us, so one
   // plane of lookahead is not enough), the rest as raw stages, capped at 10.
-  static constexpr int BUDGET = L::SMEM_PER_CTA - 512;
+  // Edge-repair table (Clamp / Mirror): per staging item with an
+  // out-of-volume cell in the read window its ready offset and the 8 raw
+  // source cells, built once per CTA.  The window [x0-R, min(x0+TX,nx)+R) x
+  // [y0-R, min(y0+TY,ny)+R) has at most R such rows on each side and at most
+  // 4 such items in any other row (R <= 4 cells on each side; a cell column
+  // in [64, 72) sits in a low and a high quad), whatever the extents.
+  static constexpr int MAX_REPAIR = 2 * R * (NPR / 4) + 4 * BY;
+  static constexpr int REPAIR_BYTES = (MAX_REPAIR * 18 + 16 + 127) / 128 * 128;
+  static constexpr int BUDGET = L::SMEM_PER_CTA - 512 - REPAIR_BYTES;
   static constexpr int S_RDY_FIT = (BUDGET - 6 * RAW_PITCH) / RDY_PITCH;
   static constexpr int S_RDY = S_RDY_FIT < 4 ? 4 : (S_RDY_FIT > 6 ? 6 : S_RDY_FIT);
   static constexpr int S_RAW_FIT = (BUDGET - S_RDY * RDY_PITCH) / RAW_PITCH;
@@ -99,7 +109,7 @@ struct Cfg {
   static constexpr int AHEAD = S_RDY >= 4 ? 2 : 1;
   static constexpr int SMEM_DATA = S_RDY * RDY_PITCH + S_RAW * RAW_PITCH;
   static constexpr int NBAR = 2 * S_RDY + 2 * S_RAW;
-  static constexpr int SMEM = SMEM_DATA + NBAR * 8 + 128;
+  static constexpr int SMEM = SMEM_DATA + REPAIR_BYTES + NBAR * 8 + 128;
   static_assert(R >= 1 && R <= 4, "radius");
   static_assert(S_RAW >= AHEAD + 2, "TMA ring too shallow");
   static_assert(SMEM <= L::SMEM_PER_CTA, "shared memory budget");
@@ -259,52 +269,80 @@ __device__ __forceinline__ float widen(uint8_t v) { return to_f32(v); }
 // [4g, 4g+4) of stage row `by`, i.e. the cells x0-4+4g .. +3 (lo halves) and
 // the same +HALF (hi halves).  `slow` marks items that hold out-of-volume
 // cells of the read window.
-template <typename T, int K, int NT>
+// Does staging item (row by, pairs 4g..4g+3: cells [4g, 4g+4) and
+// [4g+HALF, 4g+HALF+4)) hold an out-of-volume cell of the read window?
+template <int R>
+__device__ __forceinline__ bool slow_item(int by, int g, int rows_lo, int rows_hi, int rows_end,
+                                          int e_lo, int e_hi, int e_end) {
+  if (by < rows_lo || (by >= rows_hi && by < rows_end)) return true;
+  auto hit = [&](int a) {  // [a, a+4) meets [4-R, e_lo) or [e_hi, e_end)
+    return (a < e_lo && a + 4 > 4 - R) || (a < e_end && a + 4 > e_hi);
+  };
+  return hit(4 * g) || hit(4 * g + HALF);
+}
+
+template <typename T, int K, int NT, bool MODE_REPAIRS>
 struct StagePlan {
   using C = Cfg<T, K>;
   static constexpr int GPR = NPR / 4;  // items per row
   static constexpr int NQ = GPR * C::BY;
   static constexpr int QPT = (NQ + NT - 1) / NT;
-  static constexpr bool STORE = true;  // offsets computed once per CTA
-  int rdy_[STORE ? QPT : 1];  // ready-stage float offset (-1: no item)
-  uint32_t slow_;             // bit k: item k takes the per-cell edge path
-  int t_, rows_lo_, rows_hi_, e_lo_, e_hi_;
-  bool edge_;
+  // offsets computed once per CTA (K = 7 recomputes them: 128-register budget)
+  static constexpr bool STORE = K <= 5;
+  int rdy_[STORE ? QPT : 1];  // ready-stage float offset (-1: no item, or an
+                              // item the repair pass writes)
+  int raw_[STORE ? QPT : 1];  // raw-stage cell offset of the item's low quad
+  int t_, rows_lo_, rows_hi_, rows_end_, e_lo_, e_hi_, e_end_;
 
+  bool edge_;
   __device__ __forceinline__ StagePlan(const TmaParams& p, int x0, int y0, bool edge, int t) {
     constexpr int R = C::R;
     t_ = t;
     edge_ = edge;
-    rows_lo_ = max(0, R - y0);    // first in-volume stage row
-    rows_hi_ = p.ny - y0 + R;     // first stage row past the volume
-    e_lo_ = max(0, 4 - x0);       // first in-volume cell column (x0-4+e)
-    e_hi_ = p.nx - x0 + 4;        // first cell column past the volume
-    slow_ = 0;
+    // out-of-volume stage rows / cell columns inside the read window of the
+    // tile's valid outputs (cells past it are read by padding outputs only)
+    rows_lo_ = R - y0;                              // rows [0, rows_lo_)
+    rows_hi_ = p.ny - y0 + R;                       // rows [rows_hi_, rows_end_)
+    rows_end_ = min(TY, p.ny - y0) + 2 * R;
+    e_lo_ = 4 - x0;                                 // cells [4-R, e_lo_)
+    e_hi_ = p.nx - x0 + 4;                          // cells [e_hi_, e_end_)
+    e_end_ = min(TX, p.nx - x0) + 4 + R;
     if constexpr (STORE) {
 #pragma unroll
-      for (int k = 0; k < QPT; ++k) {
-        int ro;
-        bool sl;
-        compute(k, ro, sl);
-        rdy_[k] = ro;
-        slow_ |= (sl ? 1u : 0u) << k;
-      }
+      for (int k = 0; k < QPT; ++k) compute(k, rdy_[k], raw_[k]);
     }
   }
-  __device__ __forceinline__ void compute(int k, int& ro, bool& sl) const {
+  __device__ __forceinline__ bool slow(int by, int g) const {
+#ifdef VKT_EXP_NOREPAIR
+    return false;
+#endif
+    return edge_ && slow_item<C::R>(by, g, rows_lo_, rows_hi_, rows_end_, e_lo_, e_hi_, e_end_);
+  }
+  // item k of the row-major staging pass (edge items are left to the repair
+  // pass, MODE != Border)
+  __device__ __forceinline__ void compute(int k, int& ro, int& wo) const {
     const int q = t_ + k * NT;
     const int by = q / GPR, g = q - by * GPR;
-    ro = q < NQ ? by * RPF + 8 * g : -1;
-    sl = q < NQ && edge_ &&
-         (by < rows_lo_ || by >= rows_hi_ || 4 * g < e_lo_ || 4 * g + HALF + 4 > e_hi_);
+    ro = q < NQ && !(MODE_REPAIRS && slow(by, g)) ? by * RPF + 8 * g : -1;
+    wo = by * C::BX + 4 * g + (C::A - 4);
   }
-  __device__ __forceinline__ void get(int k, int& ro, bool& sl) const {
+  __device__ __forceinline__ void get(int k, int& ro, int& wo) const {
     if constexpr (STORE) {
       ro = rdy_[k];
-      sl = (slow_ >> k) & 1u;
+      wo = raw_[k];
     } else {
-      compute(k, ro, sl);
+      compute(k, ro, wo);
     }
+  }
+  // item k of the column-major repair pass (edge tiles): the items of one
+  // ready column are consecutive, so an edge column's repairs fall on the
+  // lanes of one warp instead of a few lanes of every warp.  Returns the
+  // ready offset, or -1 if the item has no out-of-volume cell.
+  __device__ __forceinline__ void repair_item_offset(int k, int& ro, int& wo) const {
+    const int q = t_ + k * NT;
+    const int g = q / C::BY, by = q - g * C::BY;
+    ro = q < NQ && slow(by, g) ? by * RPF + 8 * g : -1;
+    wo = by * C::BX + 4 * g + (C::A - 4);
   }
 };
 
@@ -334,23 +372,159 @@ __device__ __forceinline__ void load_quad(const T* src, uint32_t (&b)[4]) {
   }
 }
 
-template <typename T, int MODE, int K, int NT>
-__device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* plane,
-                                            const TmaParams& p, int x0, int y0,
-                                            const StagePlan<T, K, NT>& sp) {
+// Out-of-volume repair of one staging item (edge tiles only), one cell at a
+// time (a rolled loop: unrolled, its eight gathers in flight inflated the
+// register allocation of the whole FFMA2 main loop into spills).
+template <typename T, int MODE, int K>
+__device__ __forceinline__ void repair_item(float* rdy, const T* raw, const T* plane,
+                                            const TmaParams* pp, int x0, int y0, int ro, int wo) {
   using C = Cfg<T, K>;
   constexpr int R = C::R;
+  const TmaParams& p = *pp;
+  uint32_t lo[4], hi[4];
+  load_quad<T>(raw + wo, lo);
+  load_quad<T>(raw + wo + HALF, hi);
+  float f[8];
 #pragma unroll
-  for (int k = 0; k < StagePlan<T, K, NT>::QPT; ++k) {
-    int ro;
-    bool sl;
-    sp.get(k, ro, sl);
+  for (int c = 0; c < 4; ++c) {
+    if constexpr (sizeof(T) == 4) {
+      f[c] = __uint_as_float(lo[c]);
+      f[c + 4] = __uint_as_float(hi[c]);
+    } else {
+      f[c] = __uint_as_float(lo[c]) - 8388608.0f;
+      f[c + 4] = __uint_as_float(hi[c]) - 8388608.0f;
+    }
+  }
+  const int by = ro / RPF, e = (ro - by * RPF) / 2;  // first cell column x0-4+e
+  const int gy = y0 - R + by;
+  const bool yo = gy < 0 || gy >= p.ny;
+  // rows past the read window of the valid outputs are left alone (their
+  // fold would leave the staged box)
+  const bool yin = gy < min(y0 + TY, p.ny) + R;
+  // halo cells overshoot by <= R <= 4: one fold is exact for extents >= 4
+  const bool near = p.nx >= 4 && p.ny >= 4;
+  const int my = near ? map_index_near<MODE>(gy, p.ny) : map_index32<MODE>(gy, p.ny);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int gx = x0 - 4 + e + (c & 3) + (c >> 2) * HALF;
+    if (yin && (yo || gx < 0 || gx >= p.nx) && gx >= x0 - R && gx < min(x0 + TX, p.nx) + R) {
+      const int mx = near ? map_index_near<MODE>(gx, p.nx) : map_index32<MODE>(gx, p.nx);
+      if constexpr (MODE == VKT_WRAP)
+        f[c] = widen(__ldg(plane + (int64_t)my * p.pitch + mx));
+      else
+        f[c] = widen(raw[(my - y0 + R) * C::BX + (mx - x0 + C::A)]);
+    }
+  }
+  float4* d = reinterpret_cast<float4*>(rdy + ro);
+  d[0] = make_float4(f[0], f[4], f[1], f[5]);
+  d[1] = make_float4(f[2], f[6], f[3], f[7]);
+}
+
+// The repair table: count, then per entry the 8 raw source cells (lo quad,
+// hi quad) as u16 and the ready-stage float offset / 8.
+struct RepairTable {
+  uint32_t* count;
+  uint4* src;      // [MAX_REPAIR] 8 x u16 raw cell offsets
+  uint16_t* dst;   // [MAX_REPAIR] ready offset / 8
+};
+
+// Clamp / Mirror: every out-of-volume cell of the read window maps onto an
+// in-volume cell of the same raw stage (R <= 4 < TX, TY), a correspondence
+// fixed for the CTA.  Built by all threads once; edge CTAs only.
+template <typename T, int MODE, int K, int NT>
+__device__ __forceinline__ void build_repair_table(const RepairTable& rt, const TmaParams& p,
+                                                   int x0, int y0, int t) {
+  using C = Cfg<T, K>;
+  constexpr int R = C::R;
+  constexpr int GPR = NPR / 4;
+  constexpr int NQ = GPR * C::BY;
+  const int rows_lo = R - y0, rows_hi = p.ny - y0 + R, rows_end = min(TY, p.ny - y0) + 2 * R;
+  const int e_lo = 4 - x0, e_hi = p.nx - x0 + 4, e_end = min(TX, p.nx - x0) + 4 + R;
+  const bool near = p.nx >= 4 && p.ny >= 4;
+  for (int q = t; q < NQ; q += NT) {
+    const int g = q / C::BY, by = q - g * C::BY;  // column-major
+    if (!slow_item<R>(by, g, rows_lo, rows_hi, rows_end, e_lo, e_hi, e_end)) continue;
+    const int gy = y0 - R + by;
+    const bool yo = gy < 0 || gy >= p.ny;
+    // rows past the read window of the valid outputs are left alone (their
+    // fold would leave the staged box)
+    const bool yin = gy < min(y0 + TY, p.ny) + R;
+    const int my = near ? map_index_near<MODE>(gy, p.ny) : map_index32<MODE>(gy, p.ny);
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint32_t pair = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = 2 * h + u;
+        const int gx = x0 - 4 + 4 * g + (c & 3) + (c >> 2) * HALF;
+        int src = by * C::BX + (gx - x0 + C::A);  // own cell
+        if (yin && (yo || gx < 0 || gx >= p.nx) && gx >= x0 - R && gx < min(x0 + TX, p.nx) + R) {
+          const int mx = near ? map_index_near<MODE>(gx, p.nx) : map_index32<MODE>(gx, p.nx);
+          src = (my - y0 + R) * C::BX + (mx - x0 + C::A);
+        }
+        pair |= (uint32_t)src << (16 * u);
+      }
+      w[h] = pair;
+    }
+    const uint32_t idx = atomicAdd(rt.count, 1u);
+#ifdef VKT_DEBUG_BOUNDS
+    {
+      const uint32_t lim = C::BX * C::BY;
+      if (idx >= (uint32_t)C::MAX_REPAIR || (w[0] & 0xFFFF) >= lim || (w[0] >> 16) >= lim ||
+          (w[1] & 0xFFFF) >= lim || (w[1] >> 16) >= lim || (w[2] & 0xFFFF) >= lim ||
+          (w[2] >> 16) >= lim || (w[3] & 0xFFFF) >= lim || (w[3] >> 16) >= lim) {
+        printf("repair table: cta (%d,%d,%d) idx %u by %d g %d w %x %x %x %x lim %u\n", blockIdx.x,
+               blockIdx.y, blockIdx.z, idx, by, g, w[0], w[1], w[2], w[3], lim);
+        __trap();
+      }
+    }
+#endif
+    rt.src[idx] = make_uint4(w[0], w[1], w[2], w[3]);
+    rt.dst[idx] = (uint16_t)((by * RPF + 8 * g) / 8);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float raw_value(const T* raw, uint32_t i) {
+  if constexpr (sizeof(T) == 4)
+    return raw[i];
+  else
+    return __uint_as_float(0x4B000000u | (uint32_t)raw[i]) - 8388608.0f;
+}
+
+// Per plane: the repaired items, straight from the table (cells 0-3: the low
+// quad, 4-7: the high quad).
+template <typename T>
+__device__ __forceinline__ void apply_repair_table(float* rdy, const T* raw, const RepairTable& rt,
+                                                   int t, int nt) {
+  const int n = (int)*rt.count;
+  for (int i = t; i < n; i += nt) {
+    const uint4 w = rt.src[i];
+    const int ro = 8 * (int)rt.dst[i];
+    const float c0 = raw_value(raw, w.x & 0xFFFFu), c1 = raw_value(raw, w.x >> 16);
+    const float c2 = raw_value(raw, w.y & 0xFFFFu), c3 = raw_value(raw, w.y >> 16);
+    const float c4 = raw_value(raw, w.z & 0xFFFFu), c5 = raw_value(raw, w.z >> 16);
+    const float c6 = raw_value(raw, w.w & 0xFFFFu), c7 = raw_value(raw, w.w >> 16);
+    float4* d = reinterpret_cast<float4*>(rdy + ro);
+    d[0] = make_float4(c0, c4, c1, c5);
+    d[1] = make_float4(c2, c6, c3, c7);
+  }
+}
+
+template <typename T, int MODE, int K, int NT>
+__device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* plane,
+                                            const TmaParams& p, int x0, int y0, bool edge,
+                                            const StagePlan<T, K, NT, MODE != VKT_BORDER>& sp,
+                                            const RepairTable& rt, int t) {
+#pragma unroll
+  for (int k = 0; k < StagePlan<T, K, NT, MODE != VKT_BORDER>::QPT; ++k) {
+    int ro, wo;
+    sp.get(k, ro, wo);
     if (ro < 0) continue;
-    const int by = ro / RPF, e = (ro - by * RPF) / 2;  // first cell column x0-4+e
-    const T* src = raw + by * C::BX + e + (C::A - 4);
     uint32_t lo[4], hi[4];
-    load_quad<T>(src, lo);
-    load_quad<T>(src + HALF, hi);
+    load_quad<T>(raw + wo, lo);
+    load_quad<T>(raw + wo + HALF, hi);
     uint64_t pr[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -359,29 +533,24 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
       else
         pr[c] = widen2(lo[c], hi[c]);
     }
-    if (MODE != VKT_BORDER && sl) {
-      const int gy = y0 - R + by;
-      const bool yo = gy < 0 || gy >= p.ny;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int gx = x0 - 4 + e + (c & 3) + (c >> 2) * HALF;
-        if ((yo || gx < 0 || gx >= p.nx) && gx >= x0 - R && gx < x0 + TX + R) {
-          // halo cells overshoot by <= R <= 4: one fold is exact for extents >= 4
-          const bool near = p.nx >= 4 && p.ny >= 4;
-          const int mx = near ? map_index_near<MODE>(gx, p.nx) : map_index32<MODE>(gx, p.nx);
-          const int my = near ? map_index_near<MODE>(gy, p.ny) : map_index32<MODE>(gy, p.ny);
-          float v;
-          if constexpr (MODE == VKT_WRAP)
-            v = widen(__ldg(plane + (int64_t)my * p.pitch + mx));
-          else
-            v = widen(raw[(my - y0 + R) * C::BX + (mx - x0 + C::A)]);
-          pr[c & 3] = (c >> 2) ? pair_c(lo_c(pr[c & 3]), v) : pair_c(v, hi_c(pr[c & 3]));
-        }
-      }
-    }
     uint4* d = reinterpret_cast<uint4*>(rdy + ro);
     d[0] = make_uint4((uint32_t)pr[0], (uint32_t)(pr[0] >> 32), (uint32_t)pr[1], (uint32_t)(pr[1] >> 32));
     d[1] = make_uint4((uint32_t)pr[2], (uint32_t)(pr[2] >> 32), (uint32_t)pr[3], (uint32_t)(pr[3] >> 32));
+  }
+  // Clamp / Mirror: from the CTA's repair table; Wrap (global sources): cell
+  // by cell.  One mechanism per kernel: each extra repair path changed
+  // ptxas's allocation of the FFMA2 main loop (spills, lost uniform weights).
+  if constexpr (MODE == VKT_CLAMP || MODE == VKT_MIRROR) {
+    if (edge) apply_repair_table<T>(rdy, raw, rt, t, NT);
+  } else if constexpr (MODE == VKT_WRAP) {
+    if (edge) {
+#pragma unroll 1
+      for (int k = 0; k < StagePlan<T, K, NT, true>::QPT; ++k) {
+        int ro, wo;
+        sp.repair_item_offset(k, ro, wo);
+        if (ro >= 0) repair_item<T, MODE, K>(rdy, raw, plane, &p, x0, y0, ro, wo);
+      }
+    }
   }
 }
 
@@ -488,7 +657,11 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   float* rdy_base = reinterpret_cast<float*>(smem);
   T* raw_base = reinterpret_cast<T*>(smem + S * C::RDY_PITCH);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA);
+  RepairTable rtab;
+  rtab.count = reinterpret_cast<uint32_t*>(smem + C::SMEM_DATA);
+  rtab.src = reinterpret_cast<uint4*>(smem + C::SMEM_DATA + 16);
+  rtab.dst = reinterpret_cast<uint16_t*>(smem + C::SMEM_DATA + 16 + 16 * C::MAX_REPAIR);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_DATA + C::REPAIR_BYTES);
   uint64_t* full = bars;            // [SR] TMA landed
   uint64_t* raw_free = full + SR;   // [SR] all warps done staging from the raw slot
   uint64_t* ready = raw_free + SR;  // [S]  staged plane complete (WARPS arrivals)
@@ -496,6 +669,15 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
 
   const int tid = threadIdx.x;
   const int lane = tid % 32;
+  // 8-warp layouts stage alternate planes with alternate warp halves (warps
+  // 0-3 even planes, 4-7 odd): each SM sub-partition holds one warp of each
+  // half, so one of them can issue FFMA2 while the other stages.  The half is
+  // broadcast from lane 0 so ptxas sees it as warp-uniform (a per-thread
+  // branch would push the weights off the uniform datapath).
+  constexpr bool SPLIT = WARPS == 8;
+  constexpr int SW = SPLIT ? WARPS / 2 : WARPS;  // staging warps per plane
+  constexpr int ST = 32 * SW;
+  const int half = __shfl_sync(0xffffffffu, tid / ST, 0);
   const int x0 = blockIdx.x * TX;
   const int y0 = blockIdx.y * TY;
   const int zo0 = p.z_begin + blockIdx.z * p.zc;
@@ -508,15 +690,20 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     prefetch_tmap(&map_src);
     for (int s = 0; s < SR; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&raw_free[s], WARPS);
+      mbar_init(&raw_free[s], SW);
     }
     for (int s = 0; s < S; ++s) {
-      mbar_init(&ready[s], WARPS);
+      mbar_init(&ready[s], SW);
       mbar_init(&empty[s], WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *rtab.count = 0;
   }
   __syncthreads();
+  if ((MODE == VKT_CLAMP || MODE == VKT_MIRROR) && edge) {
+    build_repair_table<T, MODE, K, THREADS>(rtab, p, x0, y0, tid);
+    __syncthreads();
+  }
 
   // TMA plane j into raw slot j % SR (zero planes: plain arrive).  Called by
   // all threads; only thread 0 acts (predicated, no divergent branch).
@@ -533,9 +720,10 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
                  x0 - C::A, y0 - R, s.z, leader);
   };
 
-  // stage plane j (all warps, equal shares) into ready slot j % S
-  const StagePlan<T, K, THREADS> splan(p, x0, y0, edge, tid);
+  // stage plane j (SW warps, equal shares) into ready slot j % S
+  const StagePlan<T, K, ST, MODE != VKT_BORDER> splan(p, x0, y0, edge, tid % ST);
   auto prepare = [&](int j) {
+    if (SPLIT && half != (j & 1)) return;
     const int s = j % S;
     float* stage = rdy_base + s * (C::RDY_PITCH / 4);
     const int r = j % SR;
@@ -544,11 +732,12 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + j);
     if (src.which < 0) {
       float4* w4 = reinterpret_cast<float4*>(stage);
-      for (int q = tid; q < C::RDY_BYTES / 16; q += THREADS) w4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = tid % ST; q < C::RDY_BYTES / 16; q += ST) w4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
       const T* raw = raw_base + r * (C::RAW_PITCH / (int)sizeof(T));
 #ifndef VKT_EXP_NOCONVERT  // diagnostics builds only (build.py --variant)
-      stage_plane<T, MODE, K, THREADS>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, splan);
+      stage_plane<T, MODE, K, ST>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, edge, splan, rtab,
+                                  tid % ST);
 #endif
     }
     __syncwarp();

@@ -308,6 +308,12 @@ def run_ours(args):
                 pin_in[(g0 - lo) * plane_b:(g1 - lo) * plane_b].copy_(h.data.array)
     host_in = pin_in.numpy().view(fmt.dtype).reshape(hi - lo, ny, nx)
     host_out = pin_out.numpy().view(fmt.dtype).reshape(hi - lo, ny, nx)
+    # untimed warm-up: the first call grows the library's device pool (the
+    # resident padded input, > 2 GB at cfg3) — a one-time cost, not a step
+    for _ in range(min(args.warmup, 2)):
+        vk.apply_filter_host(host_in, kernel, mode, out=host_out, z_offset=lo, global_nz=nz,
+                             z_range=(src.z0 - lo, src.z1 - lo))
+    torch.cuda.synchronize()
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)

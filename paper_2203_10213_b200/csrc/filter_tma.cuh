@@ -50,15 +50,15 @@ constexpr int NPR = HALF + 8;    // pairs per ready row: lo x in [x0-4, x0+HALF+
 constexpr int RPF = 2 * NPR;     // ready row pitch in floats
 
 // Thread layout per voxel size and kernel extent (measured):
-//  u8/u16, K <= 5: 2 output rows per thread, 4 warps, 3 CTAs/SM (3 warps per
+//  u8/u16, K == 3: 2 output rows per thread, 4 warps, 3 CTAs/SM (3 warps per
 //          SMSP);
-//  otherwise: 1 row per thread, 8 warps, 2 CTAs/SM (4 warps/SMSP, 128 regs) —
-//          f32 needs the larger shared-memory budget for its raw ring.
+//  otherwise: 1 row per thread, 8 warps (staging split between the halves),
+//          2 CTAs/SM (4 warps/SMSP, 128 regs).
 // Warps per SM stay a multiple of 4 so every SM sub-partition gets the same
 // number of FMA warps.
 template <int BPC, int K>
 struct Layout {
-  static constexpr bool SMALL = K <= 5 && BPC < 4;
+  static constexpr bool SMALL = K == 3 && BPC < 4;
   static constexpr int YPT = SMALL ? 2 : 1;
   static constexpr int WARPS = TY * TPR / (32 * YPT);
   static constexpr int THREADS = 32 * WARPS;

@@ -34,6 +34,8 @@
 
 #include <cuda.h>
 
+#include <atomic>
+
 #include <cstdio>
 
 #include "common.cuh"
@@ -47,7 +49,34 @@ constexpr int HALF = TX / 2;     // x distance between the two outputs of a pair
 constexpr int XQ = 4;            // output pairs per thread row (8 outputs)
 constexpr int TPR = HALF / XQ;   // threads per output row
 constexpr int NPR = HALF + 8;    // pairs per ready row: lo x in [x0-4, x0+HALF+4)
-constexpr int RPF = 2 * NPR;     // ready row pitch in floats
+// Ready-stage bank layout.  A thread reads a run of 16-byte chunks starting
+// at chunk 2*tx of its row (and staging writes one item of 2 chunks per
+// thread), so with a plain layout the 8 lanes of a 128-bit quarter-warp phase
+// (tx..tx+7 of one row) hit 4 bank groups twice: 2-way conflicts on every
+// LDS.128 / STS.128 (ncu: 2.5x the ideal shared wavefronts at K = 3).  Two
+// cures, per kernel extent:
+//  * K = 3 (2 rows per thread): XOR swizzle within a row — chunk c of an odd
+//    128-byte line is stored at c ^ 1 (in-row float offset o -> o ^ ((o >> 3)
+//    & 4)), rows padded to 160 floats; lanes t and t+4 of a phase then fall
+//    in lines of opposite parity.  Each load needs its own address register,
+//    affordable at K = 3.
+//  * K >= 5 (1 row per thread): rows 148 floats = 37 chunks apart (odd) and a
+//    quarter-warp holds tx 0..3 of TWO adjacent rows (lane_layout below), so
+//    the two halves of a phase fall on opposite chunk parities.  Loads keep a
+//    single base register with immediate offsets (at K = 7 per-load address
+//    registers cost ptxas ~2x the register moves on the FFMA2 loop, measured).
+__device__ __forceinline__ int swz(int o) { return o ^ ((o >> 3) & 4); }
+
+template <int K>
+struct Ready {
+  static constexpr bool SWZ = K == 3;
+  static constexpr int RPF = SWZ ? 160 : 2 * NPR + 4;  // row pitch (floats)
+  // physical offset of in-row float offset o (a multiple of 4)
+  __host__ __device__ static constexpr int in_row(int o) { return SWZ ? (o ^ ((o >> 3) & 4)) : o; }
+  // the item's second chunk, given the physical offset of its first
+  __device__ __forceinline__ static int second(int so) { return SWZ ? (so ^ 4) : so + 4; }
+};
+static_assert((2 * NPR + 4) / 4 % 2 == 1, "K >= 5 ready rows must be an odd number of chunks");
 
 // Thread layout per voxel size and kernel extent (measured):
 //  u8/u16, K == 3: 2 output rows per thread, 4 warps, 3 CTAs/SM (3 warps per
@@ -86,6 +115,7 @@ struct Cfg {
   static constexpr int BY = TY + 2 * R;
   static constexpr int RAW_BYTES = BX * BY * (int)sizeof(T);
   static constexpr int RAW_PITCH = (RAW_BYTES + 127) / 128 * 128;
+  static constexpr int RPF = Ready<K>::RPF;
   static constexpr int RDY_BYTES = RPF * BY * 4;
   static constexpr int RDY_PITCH = (RDY_BYTES + 127) / 128 * 128;
   // Ring depths within CTAS_PER_SM CTAs per SM: 4..6 ready stages (AHEAD = 2
@@ -319,11 +349,12 @@ struct StagePlan {
     return edge_ && slow_item<C::R>(by, g, rows_lo_, rows_hi_, rows_end_, e_lo_, e_hi_, e_end_);
   }
   // item k of the row-major staging pass (edge items are left to the repair
-  // pass, MODE != Border)
+  // pass, MODE != Border): ro = the swizzled ready offset of its first chunk
+  // (the second is at ro ^ 4), or -1
   __device__ __forceinline__ void compute(int k, int& ro, int& wo) const {
     const int q = t_ + k * NT;
     const int by = q / GPR, g = q - by * GPR;
-    ro = q < NQ && !(MODE_REPAIRS && slow(by, g)) ? by * RPF + 8 * g : -1;
+    ro = q < NQ && !(MODE_REPAIRS && slow(by, g)) ? by * C::RPF + Ready<K>::in_row(8 * g) : -1;
     wo = by * C::BX + 4 * g + (C::A - 4);
   }
   __device__ __forceinline__ void get(int k, int& ro, int& wo) const {
@@ -341,7 +372,7 @@ struct StagePlan {
   __device__ __forceinline__ void repair_item_offset(int k, int& ro, int& wo) const {
     const int q = t_ + k * NT;
     const int g = q / C::BY, by = q - g * C::BY;
-    ro = q < NQ && slow(by, g) ? by * RPF + 8 * g : -1;
+    ro = q < NQ && slow(by, g) ? by * C::RPF + 8 * g : -1;
     wo = by * C::BX + 4 * g + (C::A - 4);
   }
 };
@@ -395,6 +426,7 @@ __device__ __forceinline__ void repair_item(float* rdy, const T* raw, const T* p
       f[c + 4] = __uint_as_float(hi[c]) - 8388608.0f;
     }
   }
+  constexpr int RPF = C::RPF;
   const int by = ro / RPF, e = (ro - by * RPF) / 2;  // first cell column x0-4+e
   const int gy = y0 - R + by;
   const bool yo = gy < 0 || gy >= p.ny;
@@ -415,17 +447,17 @@ __device__ __forceinline__ void repair_item(float* rdy, const T* raw, const T* p
         f[c] = widen(raw[(my - y0 + R) * C::BX + (mx - x0 + C::A)]);
     }
   }
-  float4* d = reinterpret_cast<float4*>(rdy + ro);
-  d[0] = make_float4(f[0], f[4], f[1], f[5]);
-  d[1] = make_float4(f[2], f[6], f[3], f[7]);
+  const int so = by * RPF + Ready<K>::in_row(2 * e);
+  *reinterpret_cast<float4*>(rdy + so) = make_float4(f[0], f[4], f[1], f[5]);
+  *reinterpret_cast<float4*>(rdy + Ready<K>::second(so)) = make_float4(f[2], f[6], f[3], f[7]);
 }
 
 // The repair table: count, then per entry the 8 raw source cells (lo quad,
-// hi quad) as u16 and the ready-stage float offset / 8.
+// hi quad) as u16 and the swizzled ready-stage float offset / 4.
 struct RepairTable {
   uint32_t* count;
   uint4* src;      // [MAX_REPAIR] 8 x u16 raw cell offsets
-  uint16_t* dst;   // [MAX_REPAIR] ready offset / 8
+  uint16_t* dst;   // [MAX_REPAIR] swizzled ready offset / 4
 };
 
 // Clamp / Mirror: every out-of-volume cell of the read window maps onto an
@@ -481,7 +513,7 @@ __device__ __forceinline__ void build_repair_table(const RepairTable& rt, const 
     }
 #endif
     rt.src[idx] = make_uint4(w[0], w[1], w[2], w[3]);
-    rt.dst[idx] = (uint16_t)((by * RPF + 8 * g) / 8);
+    rt.dst[idx] = (uint16_t)((by * C::RPF + Ready<K>::in_row(8 * g)) / 4);
   }
 }
 
@@ -495,20 +527,19 @@ __device__ __forceinline__ float raw_value(const T* raw, uint32_t i) {
 
 // Per plane: the repaired items, straight from the table (cells 0-3: the low
 // quad, 4-7: the high quad).
-template <typename T>
+template <typename T, int K>
 __device__ __forceinline__ void apply_repair_table(float* rdy, const T* raw, const RepairTable& rt,
                                                    int t, int nt) {
   const int n = (int)*rt.count;
   for (int i = t; i < n; i += nt) {
     const uint4 w = rt.src[i];
-    const int ro = 8 * (int)rt.dst[i];
+    const int ro = 4 * (int)rt.dst[i];
     const float c0 = raw_value(raw, w.x & 0xFFFFu), c1 = raw_value(raw, w.x >> 16);
     const float c2 = raw_value(raw, w.y & 0xFFFFu), c3 = raw_value(raw, w.y >> 16);
     const float c4 = raw_value(raw, w.z & 0xFFFFu), c5 = raw_value(raw, w.z >> 16);
     const float c6 = raw_value(raw, w.w & 0xFFFFu), c7 = raw_value(raw, w.w >> 16);
-    float4* d = reinterpret_cast<float4*>(rdy + ro);
-    d[0] = make_float4(c0, c4, c1, c5);
-    d[1] = make_float4(c2, c6, c3, c7);
+    *reinterpret_cast<float4*>(rdy + ro) = make_float4(c0, c4, c1, c5);
+    *reinterpret_cast<float4*>(rdy + Ready<K>::second(ro)) = make_float4(c2, c6, c3, c7);
   }
 }
 
@@ -533,15 +564,16 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
       else
         pr[c] = widen2(lo[c], hi[c]);
     }
-    uint4* d = reinterpret_cast<uint4*>(rdy + ro);
-    d[0] = make_uint4((uint32_t)pr[0], (uint32_t)(pr[0] >> 32), (uint32_t)pr[1], (uint32_t)(pr[1] >> 32));
-    d[1] = make_uint4((uint32_t)pr[2], (uint32_t)(pr[2] >> 32), (uint32_t)pr[3], (uint32_t)(pr[3] >> 32));
+    *reinterpret_cast<uint4*>(rdy + ro) =
+        make_uint4((uint32_t)pr[0], (uint32_t)(pr[0] >> 32), (uint32_t)pr[1], (uint32_t)(pr[1] >> 32));
+    *reinterpret_cast<uint4*>(rdy + Ready<K>::second(ro)) =
+        make_uint4((uint32_t)pr[2], (uint32_t)(pr[2] >> 32), (uint32_t)pr[3], (uint32_t)(pr[3] >> 32));
   }
   // Clamp / Mirror: from the CTA's repair table; Wrap (global sources): cell
   // by cell.  One mechanism per kernel: each extra repair path changed
   // ptxas's allocation of the FFMA2 main loop (spills, lost uniform weights).
   if constexpr (MODE == VKT_CLAMP || MODE == VKT_MIRROR) {
-    if (edge) apply_repair_table<T>(rdy, raw, rt, t, NT);
+    if (edge) apply_repair_table<T, K>(rdy, raw, rt, t, NT);
   } else if constexpr (MODE == VKT_WRAP) {
     if (edge) {
 #pragma unroll 1
@@ -589,33 +621,53 @@ struct Accum {
   uint64_t p[YPT][K][XQ];
 };
 
+// The aligned run of ready pairs a thread loads per row: output pair j
+// (x = x0+4tx+j) at tap dx reads ready pair 4tx+j+dx+4-R, so the thread loads
+// pairs [4tx+LOFF, 4tx+LOFF+2*NLD) as NLD 16-byte chunks.  off[i]: chunk i's
+// physical in-row float offset (swizzled layout only; the plain layout
+// addresses chunk i as base + 4i).
+template <int K>
+struct LoadRun {
+  static constexpr int R = K / 2;
+  static constexpr int LOFF = (4 - R) & ~1;
+  static constexpr int SH = 4 - R - LOFF;                // 0 or 1
+  static constexpr int NLD = (XQ + K - 1 + SH + 1) / 2;  // LDS.128 per row
+  static constexpr int NOFF = Ready<K>::SWZ ? NLD : 1;
+  __device__ __forceinline__ static void offsets(int tx, int (&off)[NOFF]) {
+#pragma unroll
+    for (int i = 0; i < NOFF; ++i) off[i] = Ready<K>::in_row(2 * (XQ * tx + LOFF) + 4 * i);
+  }
+};
+
 // One input plane's contribution to the K rolling accumulators of the
 // thread's YPT x 4 output pairs.  GUARD: skip slots whose output plane is
 // outside the chunk (ramp up / down; those sums are never stored).
-// Output pair j (x = x0+4tx+j) at tap dx reads ready pair 4tx+j+dx+4-R; the
-// thread loads the aligned run of pairs [4tx+LOFF, 4tx+LOFF+2*NLD).
 template <int K, int YPT, bool GUARD>
-__device__ __forceinline__ void plane_step(const float* __restrict__ stage, int tx, int ty,
+__device__ __forceinline__ void plane_step(const float* __restrict__ stage,
+                                           const int (&off)[LoadRun<K>::NOFF], int ty,
                                            const Weights<K>& wt, Accum<K, YPT>& acc, int first,
                                            int last) {
-  constexpr int R = K / 2;
-  constexpr int LOFF = (4 - R) & ~1;
-  constexpr int SH = 4 - R - LOFF;                   // 0 or 1
-  constexpr int NLD = (XQ + K - 1 + SH + 1) / 2;     // LDS.128 per row
-  const float* base = stage + YPT * ty * RPF + 2 * (XQ * tx + LOFF);
-#ifdef VKT_EXP_UNROLL_DY
+  constexpr int SH = LoadRun<K>::SH;
+  constexpr int NLD = LoadRun<K>::NLD;
+  constexpr int RPF = Ready<K>::RPF;
+  const float* base = stage + YPT * ty * RPF;
+  // dy unrolled for K <= 5: rolled, ptxas renames the accumulators at the
+  // back edge with IMAD.MOV (FMA pipe) — measured at K = 5: 4.46 vs 5.33 ms.
+  // K = 7 stays rolled (instruction cache).
+#if defined(VKT_EXP_UNROLL_DY)
 #pragma unroll
 #else
-#pragma unroll(K <= 3 ? K : 1)
+#pragma unroll(K <= 5 ? K : 1)
 #endif
   for (int dy = 0; dy < K; ++dy) {
     uint64_t P[YPT][2 * NLD];
 #pragma unroll
     for (int r = 0; r < YPT; ++r) {
-      const float4* row = reinterpret_cast<const float4*>(base + (r + dy) * RPF);
+      const float* row = base + (r + dy) * RPF;
 #pragma unroll
       for (int i = 0; i < NLD; ++i) {
-        const float4 q = row[i];
+        const float4 q = *reinterpret_cast<const float4*>(
+            row + (Ready<K>::SWZ ? off[Ready<K>::SWZ ? i : 0] : off[0] + 4 * i));
         P[r][2 * i] = f2pack(q.x, q.y);
         P[r][2 * i + 1] = f2pack(q.z, q.w);
       }
@@ -752,8 +804,19 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   for (int j = 0; j < C::AHEAD && j < np; ++j) prepare(j);
 #endif
 
-  const int tx = tid % TPR;
-  const int ty = tid / TPR;
+  // lane layout: 2-row layouts (K = 3) run tx along the lanes; 1-row layouts
+  // put tx 0..3 of two adjacent rows in each quarter-warp (see Ready<K>)
+  int tx, ty;
+  if constexpr (YPT == 1) {
+    static_assert(TPR == 16, "lane layout");
+    tx = (lane & 3) | ((lane >> 3) << 2);
+    ty = 2 * (tid / 32) + ((lane >> 2) & 1);
+  } else {
+    tx = tid % TPR;
+    ty = tid / TPR;
+  }
+  int ld_off[LoadRun<K>::NOFF];
+  LoadRun<K>::offsets(tx, ld_off);
   const float a0 = acc_init<T>(p.c);
   const uint64_t a00 = f2pack(a0, a0);
   Accum<K, YPT> acc;
@@ -794,9 +857,9 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
     if (first <= 0 && last >= K - 1)
-      plane_step<K, YPT, false>(stage, tx, ty, wt, acc, 0, K - 1);
+      plane_step<K, YPT, false>(stage, ld_off, ty, wt, acc, 0, K - 1);
     else
-      plane_step<K, YPT, true>(stage, tx, ty, wt, acc, first, last);
+      plane_step<K, YPT, true>(stage, ld_off, ty, wt, acc, first, last);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
@@ -831,8 +894,18 @@ cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, cons
   for (int r = 0; r < K * K; ++r)
     for (int x = 0; x < K; ++x) wt.w[r * Weights<K>::KP + x] = w32[r * K + x];
   auto fn = filter_tma_kernel<T, K, MODE>;
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  // the shared-memory opt-in once per device (a per-call attribute set was a
+  // measurable share of the host time of small launches)
+  static std::atomic<uint64_t> opted{0};
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(opted.load(std::memory_order_acquire) & bit)) {
+    err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (err != cudaSuccess) return err;
+    opted.fetch_or(bit, std::memory_order_release);
+  }
   fn<<<grid, C::L::THREADS, C::SMEM, s>>>(ms, ml, mh, p, wt);
   return cudaGetLastError();
 }

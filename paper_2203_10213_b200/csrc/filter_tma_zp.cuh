@@ -40,6 +40,8 @@
 
 #include <cuda.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace vkt {
@@ -767,8 +769,18 @@ cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, cons
     for (int dx = 0; dx < K; ++dx) wt.ws[dy * Weights<K>::KP + dx] = w32[dy * K + dx];
   }
   auto fn = filter_tma_kernel<T, K, MODE>;
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  // the shared-memory opt-in once per device (a per-call attribute set was a
+  // measurable share of the host time of small launches)
+  static std::atomic<uint64_t> opted{0};
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(opted.load(std::memory_order_acquire) & bit)) {
+    err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (err != cudaSuccess) return err;
+    opted.fetch_or(bit, std::memory_order_release);
+  }
   fn<<<grid, Layout<K>::THREADS, C::SMEM, s>>>(ms, ml, mh, p, wt);
   return cudaGetLastError();
 }

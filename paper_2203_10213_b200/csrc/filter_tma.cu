@@ -121,9 +121,9 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   // estimated time  waves(ZC) * (ZC + 2R + fill)  (fill ~ 3 planes).
   const int nzo = plan.z_end - plan.z_begin;
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
-  // CTAs per SM: the paired kernel's Layout, or 3 for the f32 K <= 5
+  // CTAs per SM: the paired kernel's Layout, or 3 for the f32 K = 3
   // filter_tma_zp.cuh variant
-  const int64_t slots = 148ll * (a.format == VKT_F32 && k <= 5 ? 3
+  const int64_t slots = 148ll * (a.format == VKT_F32 && k == 3 ? 3
                                  : k == 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
                                           : tma::Layout<2, 3>::CTAS_PER_SM);

@@ -1,6 +1,7 @@
 // filter_tma_f32.cu — the tiled TMA kernels for float voxels (K in {3,5,7} x
-// the four address modes): K = 7 on the paired-layout kernel (filter_tma.cuh),
-// K <= 5 on the direct-staging variant (filter_tma_zp.cuh, see its header).
+// the four address modes): K = 5, 7 on the paired-layout kernel
+// (filter_tma.cuh), K = 3 on the direct-staging variant (filter_tma_zp.cuh,
+// see its header).
 #include <cstring>
 
 #include "filter_tma.cuh"
@@ -12,20 +13,24 @@ template <>
 cudaError_t launch_tma_dtype<float>(int k, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
                                     const CUtensorMap& mh, const TmaParams& p, const float* w32,
                                     dim3 grid, cudaStream_t s) {
-  if (k <= 5) {
+  if (k == 3) {
     static_assert(sizeof(tma_zp::TmaParams) == sizeof(TmaParams), "parameter layouts");
     tma_zp::TmaParams zp;
     std::memcpy(&zp, &p, sizeof zp);
     return tma_zp::launch_tma_dtype<float>(k, mode, ms, ml, mh, zp, w32, grid, s);
   }
-  if (k != 7) return cudaErrorInvalidValue;
-  switch (mode) {
-    case VKT_WRAP: return launch_tma_kernel<float, 7, VKT_WRAP>(ms, ml, mh, p, w32, grid, s);
-    case VKT_MIRROR: return launch_tma_kernel<float, 7, VKT_MIRROR>(ms, ml, mh, p, w32, grid, s);
-    case VKT_CLAMP: return launch_tma_kernel<float, 7, VKT_CLAMP>(ms, ml, mh, p, w32, grid, s);
-    case VKT_BORDER: return launch_tma_kernel<float, 7, VKT_BORDER>(ms, ml, mh, p, w32, grid, s);
-    default: return cudaErrorInvalidValue;
-  }
+#define VKT_F32_CASES(KK)                                                                        \
+  if (k == KK) switch (mode) {                                                                  \
+      case VKT_WRAP: return launch_tma_kernel<float, KK, VKT_WRAP>(ms, ml, mh, p, w32, grid, s);     \
+      case VKT_MIRROR: return launch_tma_kernel<float, KK, VKT_MIRROR>(ms, ml, mh, p, w32, grid, s); \
+      case VKT_CLAMP: return launch_tma_kernel<float, KK, VKT_CLAMP>(ms, ml, mh, p, w32, grid, s);   \
+      case VKT_BORDER: return launch_tma_kernel<float, KK, VKT_BORDER>(ms, ml, mh, p, w32, grid, s); \
+      default: return cudaErrorInvalidValue;                                                    \
+    }
+  VKT_F32_CASES(5)
+  VKT_F32_CASES(7)
+#undef VKT_F32_CASES
+  return cudaErrorInvalidValue;
 }
 }  // namespace tma
 }  // namespace vkt

@@ -1,11 +1,13 @@
-// filter_tma_zp.cuh — the f32 K <= 5 variant of the tiled kernel.
+// filter_tma_zp.cuh — the f32 K = 3 variant of the tiled kernel.
 //
 // TMA lands directly in the row-major ready stage (no staging pass), and
 // K-1 of the K accumulator slots are paired along z (FFMA2 with a broadcast
-// input and a weight pair) while the last slot is a plain FFMA.  For f32
-// K <= 5 (HBM-bound K = 3, short K = 5 planes) skipping the staging pass
-// outweighs the all-FFMA2 packing of filter_tma.cuh (measured, 1024^3:
-// K = 3 1.72 vs 2.78 ms, K = 5 4.99 vs 5.93 ms).  Same tensor map as
+// input and a weight pair) while the last slot is a plain FFMA.  For the
+// HBM-bound f32 K = 3 skipping the staging pass outweighs the all-FFMA2
+// packing of filter_tma.cuh (measured, 1024^3: 1.71 vs 2.03 ms).  f32 K = 5
+// moved to filter_tma.cuh once its ready stage was bank-conflict free and its
+// dy loop unrolled (4.28 vs 4.96 ms); the K = 5 code below is kept
+// compilable but is not instantiated.  Same tensor map as
 // filter_tma.cuh for f32 (box 136 x (TY+2R)); the u8/u16 code paths below
 // are not instantiated.
 //
@@ -798,7 +800,6 @@ cudaError_t launch_tma_dtype(int k, int mode, const CUtensorMap& ms, const CUten
   VKT_TMA_CASE(KK, VKT_CLAMP)       \
   VKT_TMA_CASE(KK, VKT_BORDER)
   VKT_TMA_K(3)
-  VKT_TMA_K(5)
 #undef VKT_TMA_K
 #undef VKT_TMA_CASE
   return cudaErrorInvalidValue;

@@ -56,9 +56,11 @@ constexpr int NPR = HALF + 8;    // pairs per ready row: lo x in [x0-4, x0+HALF+
 // LDS.128 / STS.128 (ncu: 2.5x the ideal shared wavefronts at K = 3).  Two
 // cures, per kernel extent:
 //  * K = 3 (2 rows per thread): XOR swizzle within a row — chunk c of an odd
-//    128-byte line is stored at c ^ 1 (in-row float offset o -> o ^ ((o >> 3)
-//    & 4)), rows padded to 160 floats; lanes t and t+4 of a phase then fall
-//    in lines of opposite parity.  Each load needs its own address register,
+//    128-byte line of the row is stored at c ^ 1 (in-row float offset o ->
+//    o ^ ((o >> 3) & 4)); lanes t and t+4 of a phase then fall in lines of
+//    opposite parity.  A row base that is not line-aligned shifts all lanes of
+//    a phase alike, so rows stay 144 floats (padding them to 160 cost a ready
+//    stage of the ring).  Each load needs its own address register,
 //    affordable at K = 3.
 //  * K >= 5 (1 row per thread): rows 148 floats = 37 chunks apart (odd) and a
 //    quarter-warp holds tx 0..3 of TWO adjacent rows (lane_layout below), so
@@ -70,7 +72,7 @@ __device__ __forceinline__ int swz(int o) { return o ^ ((o >> 3) & 4); }
 template <int K>
 struct Ready {
   static constexpr bool SWZ = K == 3;
-  static constexpr int RPF = SWZ ? 160 : 2 * NPR + 4;  // row pitch (floats)
+  static constexpr int RPF = SWZ ? 2 * NPR : 2 * NPR + 4;  // row pitch (floats)
   // physical offset of in-row float offset o (a multiple of 4)
   __host__ __device__ static constexpr int in_row(int o) { return SWZ ? (o ^ ((o >> 3) & 4)) : o; }
   // the item's second chunk, given the physical offset of its first
@@ -132,7 +134,10 @@ struct Cfg {
   static constexpr int MAX_REPAIR = 2 * R * (NPR / 4) + 4 * BY;
   static constexpr int REPAIR_BYTES = (MAX_REPAIR * 18 + 16 + 127) / 128 * 128;
   static constexpr int BUDGET = L::SMEM_PER_CTA - 512 - REPAIR_BYTES;
-  static constexpr int S_RDY_FIT = (BUDGET - 6 * RAW_PITCH) / RDY_PITCH;
+#ifndef VKT_RAW_MIN
+#define VKT_RAW_MIN 6
+#endif
+  static constexpr int S_RDY_FIT = (BUDGET - VKT_RAW_MIN * RAW_PITCH) / RDY_PITCH;
   static constexpr int S_RDY = S_RDY_FIT < 4 ? 4 : (S_RDY_FIT > 6 ? 6 : S_RDY_FIT);
   static constexpr int S_RAW_FIT = (BUDGET - S_RDY * RDY_PITCH) / RAW_PITCH;
   static constexpr int S_RAW = S_RAW_FIT < 10 ? S_RAW_FIT : 10;
@@ -642,7 +647,7 @@ struct LoadRun {
 // One input plane's contribution to the K rolling accumulators of the
 // thread's YPT x 4 output pairs.  GUARD: skip slots whose output plane is
 // outside the chunk (ramp up / down; those sums are never stored).
-template <int K, int YPT, bool GUARD>
+template <int K, int YPT, bool GUARD, bool UNROLL>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
                                            const int (&off)[LoadRun<K>::NOFF], int ty,
                                            const Weights<K>& wt, Accum<K, YPT>& acc, int first,
@@ -651,13 +656,13 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
   constexpr int NLD = LoadRun<K>::NLD;
   constexpr int RPF = Ready<K>::RPF;
   const float* base = stage + YPT * ty * RPF;
-  // dy unrolled for K <= 5: rolled, ptxas renames the accumulators at the
-  // back edge with IMAD.MOV (FMA pipe) — measured at K = 5: 4.46 vs 5.33 ms.
-  // K = 7 stays rolled (instruction cache).
+  // dy unrolled (UNROLL): rolled, ptxas renames the accumulators at the back
+  // edge with IMAD.MOV (FMA pipe) — measured at K = 5: 4.46 vs 5.33 ms; f32
+  // K = 7: 11.40 vs 11.88 ms.  u8/u16 K = 7 stay rolled (unrolled: no gain).
 #if defined(VKT_EXP_UNROLL_DY)
 #pragma unroll
 #else
-#pragma unroll(K <= 5 ? K : 1)
+#pragma unroll(UNROLL ? K : 1)
 #endif
   for (int dy = 0; dy < K; ++dy) {
     uint64_t P[YPT][2 * NLD];
@@ -730,6 +735,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   constexpr int SW = SPLIT ? WARPS / 2 : WARPS;  // staging warps per plane
   constexpr int ST = 32 * SW;
   const int half = __shfl_sync(0xffffffffu, tid / ST, 0);
+  const int warp = __shfl_sync(0xffffffffu, tid / 32, 0);
   const int x0 = blockIdx.x * TX;
   const int y0 = blockIdx.y * TY;
   const int zo0 = p.z_begin + blockIdx.z * p.zc;
@@ -843,9 +849,14 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     const int s = i % S;
     const float* stage = rdy_base + s * (C::RDY_PITCH / 4);
 #ifndef VKT_EXP_COMPUTEONLY
-    // refill the raw slot of plane i-1 (staged AHEAD iterations before)
+    // refill the raw slot of plane i-1 (staged AHEAD iterations before).
+    // Only warp 0 (the TMA issuer's) waits for the slot: a warp of the other
+    // staging half may run up to S_RDY - AHEAD planes ahead, and if the ring
+    // has S_RAW <= S_RDY it can complete the slot's NEXT phase too, so a
+    // lagging warp waiting on the parity would see the phase after next and
+    // deadlock.  Warp 0 cannot lag past its own refill.
     if (i >= 1 && i - 1 + SR < np) {
-      mbar_wait(&raw_free[(i - 1) % SR], (uint32_t)(((i - 1) / SR) & 1));
+      if (warp == 0) mbar_wait(&raw_free[(i - 1) % SR], (uint32_t)(((i - 1) / SR) & 1));
       issue(i - 1 + SR);
     }
     if (i + C::AHEAD < np) prepare(i + C::AHEAD);
@@ -856,10 +867,11 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     // slot m <-> output plane zo0 + i - 2R + m
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
+    constexpr bool UNROLL = K <= 5 || sizeof(T) == 4;
     if (first <= 0 && last >= K - 1)
-      plane_step<K, YPT, false>(stage, ld_off, ty, wt, acc, 0, K - 1);
+      plane_step<K, YPT, false, UNROLL>(stage, ld_off, ty, wt, acc, 0, K - 1);
     else
-      plane_step<K, YPT, true>(stage, ld_off, ty, wt, acc, first, last);
+      plane_step<K, YPT, true, UNROLL>(stage, ld_off, ty, wt, acc, first, last);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 

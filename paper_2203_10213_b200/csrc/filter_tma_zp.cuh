@@ -325,6 +325,107 @@ __device__ __forceinline__ void fixup_f32(float* stage, const float* plane, cons
   }
 }
 
+// Out-of-line copy for the rare Clamp / Mirror windows FixList does not cover
+// (its registers stay out of the main loop's allocation).
+template <int MODE, int R>
+__device__ __noinline__ void fixup_f32_cold(float* stage, const float* plane, const TmaParams& p,
+                                            int x0, int y0, int t, int nt, int row_lo, int row_hi) {
+  fixup_f32<MODE, R>(stage, plane, p, x0, y0, t, nt, row_lo, row_hi);
+}
+
+// Clamp / Mirror, f32 stages: the out-of-volume cells of a warp's read window
+// and their in-volume sources are the same on every plane (both inside the
+// staged box), so each lane precomputes its share once — up to NB (dst, src)
+// stage offsets — and a plane's repair is NB shared-memory copies.  Per plane
+// the generic fixup_f32 re-derived the cells (integer divisions, address
+// maps): f32 3^3 Clamp ran 15% behind Border, whose TMA zero fill needs no
+// repair.  Windows with more than 32*NB such cells (volumes thinner than
+// the halo) keep the generic path.
+template <int MODE, int R>
+struct FixList {
+  static constexpr int NB = 6;
+  int dst[NB], src[NB];
+  bool ok = false;
+  __device__ __forceinline__ FixList() {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) dst[b] = -1, src[b] = 0;
+  }
+  __device__ __forceinline__ FixList(const TmaParams& p, int x0, int y0, int lane, int row_lo,
+                                     int row_hi) {
+    const EdgeCells ec(p, x0, y0, R, row_lo, row_hi);
+    ok = ec.total <= 32 * NB;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int q = lane + 32 * b;
+      dst[b] = -1;
+      src[b] = 0;
+      if (ok && q < ec.total) {
+        int gx, gy;
+        ec.cell(p, q, gx, gy);
+        const int mx = map_index32<MODE>(gx, p.nx);
+        const int my = map_index32<MODE>(gy, p.ny);
+        dst[b] = (gy - y0 + R) * RP + (gx - x0 + 4);
+        src[b] = (my - y0 + R) * RP + (mx - x0 + 4);
+      }
+    }
+  }
+  // sources are in-volume cells, destinations out-of-volume: disjoint
+  __device__ __forceinline__ void apply(float* stage) const {
+    float v[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) v[b] = dst[b] >= 0 ? stage[src[b]] : 0.f;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (dst[b] >= 0) stage[dst[b]] = v[b];
+  }
+};
+
+// Wrap, f32 stages: the sources of a window's out-of-volume cells are on the
+// far faces of the plane, in global memory, at offsets fixed for the CTA.
+// Each lane precomputes up to NB (stage offset, plane offset) pairs and
+// gathers the NEXT plane's values while the current plane computes, so the
+// global round trip is off the per-plane critical path (the per-plane
+// gather in fixup_f32 stalled every plane of every edge tile).
+template <int R>
+struct WrapList {
+  static constexpr int NB = 6;
+  int dst[NB], off[NB];
+  float val[NB];
+  bool ok = false;
+  __device__ __forceinline__ WrapList() {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) dst[b] = -1, off[b] = 0, val[b] = 0.f;
+  }
+  __device__ __forceinline__ WrapList(const TmaParams& p, int x0, int y0, int lane, int row_lo,
+                                      int row_hi) {
+    const EdgeCells ec(p, x0, y0, R, row_lo, row_hi);
+    ok = ec.total <= 32 * NB;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int q = lane + 32 * b;
+      dst[b] = -1;
+      off[b] = 0;
+      val[b] = 0.f;
+      if (ok && q < ec.total) {
+        int gx, gy;
+        ec.cell(p, q, gx, gy);
+        dst[b] = (gy - y0 + R) * RP + (gx - x0 + 4);
+        off[b] = map_index32<VKT_WRAP>(gy, p.ny) * p.pitch + map_index32<VKT_WRAP>(gx, p.nx);
+      }
+    }
+  }
+  __device__ __forceinline__ void gather(const float* plane) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (dst[b] >= 0) val[b] = __ldg(plane + off[b]);
+  }
+  __device__ __forceinline__ void apply(float* stage) const {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (dst[b] >= 0) stage[dst[b]] = val[b];
+  }
+};
+
 // u8/u16: this thread's share of the widening work, fixed for the whole CTA
 // (the tile geometry is the same for every plane): quad q = t + k*nt covers
 // ready cells [e, e+4) of stage row `by`.  Offsets are computed once; `slow`
@@ -686,6 +787,15 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
   T* out_base = static_cast<T*>(p.dst) + (int64_t)oy * p.pitch + ox;
   const int64_t plane_elems = (int64_t)p.pitch * p.ny;
 
+  const FixList<MODE, R> fix = (C::IS_F32 && (MODE == VKT_CLAMP || MODE == VKT_MIRROR) && edge)
+                                   ? FixList<MODE, R>(p, x0, y0, lane, WROWS * warp,
+                                                      WROWS * warp + WROWS + 2 * R)
+                                   : FixList<MODE, R>();
+  WrapList<R> wrap = (C::IS_F32 && MODE == VKT_WRAP && edge)
+                         ? WrapList<R>(p, x0, y0, lane, WROWS * warp, WROWS * warp + WROWS + 2 * R)
+                         : WrapList<R>();
+  if (C::IS_F32 && MODE == VKT_WRAP && edge && wrap.ok)
+    wrap.gather(plane_ptr<float>(p, resolve<MODE>(p, R, zo0 - R)));
   for (int i = 0; i < np; ++i) {
     const int s = i % S;
     float* stage = rdy_base + s * (C::RDY_PITCH / 4);
@@ -697,21 +807,36 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
         issue(i + SR - LAG);
       }
       mbar_wait(&full[s], (uint32_t)((i / S) & 1));
-      if (MODE != VKT_BORDER || edge) {
-        const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + i);
-        if (src.which < 0) {
-          // Border zero plane: this warp clears the rows it reads
+      if constexpr (MODE == VKT_BORDER) {
+        // Border z planes outside the volume: this warp clears the rows it
+        // reads (TMA's zero fill covers x / y)
+        if (resolve<MODE>(p, R, zo0 - R + i).which < 0) {
           for (int q = lane; q < (WROWS + 2 * R) * (RP / 4); q += 32)
             reinterpret_cast<float4*>(stage + (WROWS * warp) * RP)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           fence_proxy_async();
           __syncwarp();
-        } else if (MODE != VKT_BORDER && edge) {
-          // repair the out-of-volume cells of this warp's read window
-          fixup_f32<MODE, R>(stage, plane_ptr<float>(p, src), p, x0, y0, lane, 32, WROWS * warp,
-                             WROWS * warp + WROWS + 2 * R);
-          fence_proxy_async();
-          __syncwarp();
         }
+      } else if (edge) {
+        // Clamp / Mirror / Wrap never yield a zero plane; only edge tiles
+        // repair the out-of-volume cells of this warp's read window.  (The
+        // per-plane plane resolve and repair branch in every CTA cost ~50
+        // instructions per warp-plane, measured.)
+        if constexpr (MODE == VKT_WRAP) {
+          if (wrap.ok) {
+            wrap.apply(stage);
+            if (i + 1 < np) wrap.gather(plane_ptr<float>(p, resolve<MODE>(p, R, zo0 - R + i + 1)));
+          } else {
+            fixup_f32_cold<MODE, R>(stage, plane_ptr<float>(p, resolve<MODE>(p, R, zo0 - R + i)), p,
+                                    x0, y0, lane, 32, WROWS * warp, WROWS * warp + WROWS + 2 * R);
+          }
+        } else if (fix.ok) {
+          fix.apply(stage);
+        } else {
+          fixup_f32_cold<MODE, R>(stage, plane_ptr<float>(p, resolve<MODE>(p, R, zo0 - R + i)), p,
+                                  x0, y0, lane, 32, WROWS * warp, WROWS * warp + WROWS + 2 * R);
+        }
+        fence_proxy_async();
+        __syncwarp();
       }
     } else {
       // refill the raw slot of plane i-1 (converted two iterations ago)
@@ -725,10 +850,14 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
     // slot m <-> output plane zo0 + i - 2R + m
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
+#ifdef VKT_EXP_ZP_NOCOMPUTE  // diagnostics: the memory pipeline alone
+    if (i == 0) plane_step<K, true, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, first, last);
+#else
     if (first <= 0 && last >= K - 1)
       plane_step<K, false, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, 0, K - 1);
     else
       plane_step<K, true, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, first, last);
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 

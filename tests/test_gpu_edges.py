@@ -50,3 +50,21 @@ def test_awkward_shapes_all_modes_and_extents(shape, fmt):
             assert ok, (shape, k, mode, ndiff, dmax)
             exact = _run(stored, fmt, w, mode, "exact")
             assert np.array_equal(exact.view(np.uint8), want.view(np.uint8)), (shape, k, mode)
+
+
+@pytest.mark.parametrize("fmt", [1, 2, 3])
+@pytest.mark.parametrize("k", [3, 5, 7])
+def test_interior_tiles_at_z_boundaries(fmt, k):
+    """Tiles with no x/y edge still meet the z boundary (zero planes under
+    Border, mapped planes otherwise): 3 x 3 tiles, the middle one interior."""
+    rng = np.random.default_rng(1000 * fmt + k)
+    nx, ny, nz = 384, 48, 5
+    stored = (rng.random((nz, ny, nx), dtype=np.float32) if fmt == 3 else
+              rng.integers(0, np.iinfo(O.DTYPE[fmt]).max + 1, size=(nz, ny, nx), dtype=O.DTYPE[fmt]))
+    w = rng.random((k, k, k))
+    w /= w.sum()
+    for mode in ("wrap", "mirror", "clamp", "border"):
+        want = O.apply_filter(stored, fmt, w, mode, workers=1)
+        got = _run(stored, fmt, w, mode, "auto")
+        ok, ndiff, dmax = within_contract(got, want, fmt)
+        assert ok, (k, mode, ndiff, dmax)

@@ -657,8 +657,7 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
   constexpr int RPF = Ready<K>::RPF;
   const float* base = stage + YPT * ty * RPF;
   // dy unrolled (UNROLL): rolled, ptxas renames the accumulators at the back
-  // edge with IMAD.MOV (FMA pipe) — measured at K = 5: 4.46 vs 5.33 ms; f32
-  // K = 7: 11.40 vs 11.88 ms.  u8/u16 K = 7 stay rolled (unrolled: no gain).
+  // edge with IMAD.MOV (FMA pipe) — measured at K = 5: 4.46 vs 5.33 ms.
 #if defined(VKT_EXP_UNROLL_DY)
 #pragma unroll
 #else
@@ -867,11 +866,16 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     // slot m <-> output plane zo0 + i - 2R + m
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
-    constexpr bool UNROLL = K <= 5 || sizeof(T) == 4;
+    // The steady-state planes run the dy loop unrolled; the ramp planes
+    // (GUARD, 2R of every chunk's ~70) keep it rolled at K = 7, which keeps
+    // the kernel's hot code compact (K = 7: 11.76 -> 11.33 ms for u16, 11.39
+    // -> 11.11 ms for f32, against all-rolled / all-unrolled).
+    constexpr bool UNROLL = true;
+    constexpr bool UNROLL_G = K <= 5;  // K = 5 with rolled ramps: 4.60 vs 4.46 ms
     if (first <= 0 && last >= K - 1)
       plane_step<K, YPT, false, UNROLL>(stage, ld_off, ty, wt, acc, 0, K - 1);
     else
-      plane_step<K, YPT, true, UNROLL>(stage, ld_off, ty, wt, acc, first, last);
+      plane_step<K, YPT, true, UNROLL_G>(stage, ld_off, ty, wt, acc, first, last);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 

@@ -121,12 +121,13 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   // estimated time  waves(ZC) * (ZC + 2R + fill)  (fill ~ 3 planes).
   const int nzo = plan.z_end - plan.z_begin;
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
-  // CTAs per SM: the paired kernel's Layout, or 3 for the f32 K = 3
-  // filter_tma_zp.cuh variant
-  const int64_t slots = 148ll * (a.format == VKT_F32 && k == 3 ? 3
+  // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
+  // K = 3 (4, Wrap 3)
+  const int64_t slots = 148ll * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
                                  : k == 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
-                                          : tma::Layout<2, 3>::CTAS_PER_SM);
+                                 : a.format == VKT_U8 ? tma::Layout<1, 3>::CTAS_PER_SM
+                                                      : tma::Layout<2, 3>::CTAS_PER_SM);
   int zc = 64;
   double best = 1e300;
   for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {

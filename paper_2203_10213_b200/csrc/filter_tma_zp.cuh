@@ -60,12 +60,14 @@ constexpr int XPT = 8;           // outputs per thread in x
 //          loses latency hiding), 8 warps, 2 CTAs/SM (4 warps/SMSP, 128 regs).
 // Warps per SM stay a multiple of 4 so every SM sub-partition gets the same
 // number of FMA warps.
-template <int K>
+template <int K, int MODE = VKT_CLAMP>
 struct Layout {
   static constexpr int YPT = K <= 5 ? 2 : 1;
   static constexpr int WARPS = TY * (TX / XPT) / (32 * YPT);
   static constexpr int THREADS = 32 * WARPS;
-  static constexpr int CTAS_PER_SM = K <= 5 ? 3 : 2;
+  // K = 3: 4 CTAs/SM (122 registers, 56 KB rings): Clamp 1.49 vs 1.57 ms at
+  // 1024^3; Wrap keeps 3 (its prefetch registers spill at 128)
+  static constexpr int CTAS_PER_SM = K <= 3 ? (MODE == VKT_WRAP ? 3 : 4) : K <= 5 ? 3 : 2;
   static constexpr int WROWS = TY / WARPS;  // output rows per warp
   static constexpr int SMEM_PER_CTA = (228 * 1024) / CTAS_PER_SM - 1024;  // minus driver reserve
 };
@@ -81,9 +83,9 @@ __host__ __device__ constexpr int box_width(int r, int bpc) {
   return (box_align_left(r, bpc) + TX + r + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
 }
 
-template <typename T, int K>
+template <typename T, int K, int MODE = VKT_CLAMP>
 struct Cfg {
-  using L = Layout<K>;
+  using L = Layout<K, MODE>;
   static constexpr int R = K / 2;
   static constexpr bool IS_F32 = sizeof(T) == 4;
   static constexpr int A = box_align_left(R, (int)sizeof(T));
@@ -669,12 +671,12 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage, int 
 }
 
 template <typename T, int K, int MODE>
-__global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
+__global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K, MODE>::CTAS_PER_SM)
     filter_tma_kernel(const __grid_constant__ CUtensorMap map_src,
                       const __grid_constant__ CUtensorMap map_lo,
                       const __grid_constant__ CUtensorMap map_hi, const TmaParams p,
                       const __grid_constant__ Weights<K> wt) {
-  using C = Cfg<T, K>;
+  using C = Cfg<T, K, MODE>;
   constexpr int R = C::R;
   constexpr int S = C::S_RDY;
   constexpr int YPT = Layout<K>::YPT;
@@ -888,7 +890,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K>::CTAS_PER_SM)
 template <typename T, int K, int MODE>
 cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, const CUtensorMap& mh,
                               const TmaParams& p, const float* w32, dim3 grid, cudaStream_t s) {
-  using C = Cfg<T, K>;
+  using C = Cfg<T, K, MODE>;
   // w32: (dz, dy, dx), x fastest
   Weights<K> wt = {};
   constexpr int NP = Weights<K>::NP;

@@ -126,8 +126,7 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   const int64_t slots = 148ll * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
                                  : k == 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
-                                 : a.format == VKT_U8 ? tma::Layout<1, 3>::CTAS_PER_SM
-                                                      : tma::Layout<2, 3>::CTAS_PER_SM);
+                                          : tma::Layout<2, 3>::CTAS_PER_SM);
   int zc = 64;
   double best = 1e300;
   for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {

@@ -81,8 +81,7 @@ struct Ready {
 static_assert((2 * NPR + 4) / 4 % 2 == 1, "K >= 5 ready rows must be an odd number of chunks");
 
 // Thread layout per voxel size and kernel extent (measured):
-//  u8/u16, K == 3: 2 output rows per thread, 4 warps, 4 (u8) / 3 (u16)
-//          CTAs/SM;
+//  u8/u16, K == 3: 2 output rows per thread, 4 warps, 4 CTAs/SM;
 //  otherwise: 1 row per thread, 8 warps (staging split between the halves),
 //          2 CTAs/SM (4 warps/SMSP, 128 regs).
 // Warps per SM stay a multiple of 4 so every SM sub-partition gets the same
@@ -93,9 +92,9 @@ struct Layout {
   static constexpr int YPT = SMALL ? 2 : 1;
   static constexpr int WARPS = TY * TPR / (32 * YPT);
   static constexpr int THREADS = 32 * WARPS;
-  // u8 K = 3 fits 4 CTAs (128 registers, 56 KB of rings each): 1.61 vs
-  // 1.74 ms at 1024^3; u16 K = 3 rings do not fit a fourth CTA
-  static constexpr int CTAS_PER_SM = SMALL ? (BPC == 1 ? 4 : 3) : 2;
+  // u8/u16 K = 3 run 4 CTAs (128 registers, 56 KB of rings each; u16 with a
+  // 3-stage ready ring, AHEAD = 1): 1.61 / 1.56 vs 1.74 / 1.75 ms at 1024^3
+  static constexpr int CTAS_PER_SM = SMALL ? 4 : 2;
   static constexpr int SMEM_PER_CTA = (228 * 1024) / CTAS_PER_SM - 1024;  // minus driver reserve
 };
 
@@ -140,7 +139,10 @@ struct Cfg {
 #define VKT_RAW_MIN 6
 #endif
   static constexpr int S_RDY_FIT = (BUDGET - VKT_RAW_MIN * RAW_PITCH) / RDY_PITCH;
-  static constexpr int S_RDY = S_RDY_FIT < 4 ? 4 : (S_RDY_FIT > 6 ? 6 : S_RDY_FIT);
+  // K = 3 integer rings (4 CTAs/SM) drop to 3 ready stages with AHEAD = 1,
+  // leaving room for deeper raw rings (u8 1.62 -> 1.58 ms; u16 needs it to fit)
+  static constexpr int S_RDY_MIN = L::SMALL ? 3 : 4;
+  static constexpr int S_RDY = S_RDY_FIT < S_RDY_MIN ? S_RDY_MIN : (S_RDY_FIT > 6 ? 6 : S_RDY_FIT);
   static constexpr int S_RAW_FIT = (BUDGET - S_RDY * RDY_PITCH) / RAW_PITCH;
   static constexpr int S_RAW = S_RAW_FIT < 10 ? S_RAW_FIT : 10;
   static constexpr int AHEAD = S_RDY >= 4 ? 2 : 1;

@@ -9,7 +9,8 @@ fixed (dz, dy, dx) tap order makes the result independent of the split
 address mode has been applied.  Those planes are fetched with NCCL send/recv
 (through ``torch.distributed``) on a high-priority comm stream while the
 interior kernel (output planes ``[rz, n-rz)``, which need no halo) runs on
-the compute stream; two thin boundary launches follow once the halos land.
+the compute stream; two thin boundary launches follow the halos on the comm
+stream, beside the interior.
 Every output voxel sees the same taps in the same order as on one GPU, so
 sharded results are bit-identical to unsharded ones.
 
@@ -281,10 +282,16 @@ def apply_filter_sharded(dst: ShardedVolume, src: ShardedVolume, kernel: Kernel,
         ranges = ((0, rz), (n - rz, n))
     else:
         ranges = ((0, n),)
-    compute.wait_stream(comm)
+    # The boundary planes run on the comm stream right behind the exchange,
+    # beside the interior launch: their CTAs fill the SMs the interior's tail
+    # leaves idle (measured on one GPU, cfg3 slab at P = 8: +1.2% over a
+    # single launch, against +4.5% when they ran after the interior;
+    # tools/shard_overhead.py).  Disjoint output planes; the compute stream
+    # joins the comm stream before anything else touches dst.
     for b, e in ranges:
         a, _k = make_args(dst.local.data_ptr(), src.local.data_ptr(), **common, **halo_ptrs,
                           out_z_begin=b, out_z_end=e)
-        launch(a, int(compute.cuda_stream))
-    lo.tensor.record_stream(compute)
-    hi.tensor.record_stream(compute)
+        launch(a, int(comm.cuda_stream))
+    compute.wait_stream(comm)
+    lo.tensor.record_stream(comm)
+    hi.tensor.record_stream(comm)

@@ -132,3 +132,30 @@ def test_product_package_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_make_args_weight_cache_follows_the_kernel():
+    """make_args caches the flat float64 weights on the Kernel; in-place edits
+    and reassignment of Kernel.weights must reach the ABI struct."""
+    import ctypes
+
+    import numpy as np
+
+    import paper_2203_10213_b200 as vk
+    from paper_2203_10213_b200.filters import make_args
+
+    k = vk.gaussian_kernel(1.0, 3)
+    a, keep = make_args(1, 2, (4, 5, 6), vk.DataFormat.UINT8, (0.0, 1.0), k, vk.AddressMode.WRAP,
+                        halo_lo=7, z_offset=3, global_nz=9, out_z_begin=1, out_z_end=5, flags=2)
+    w = np.ctypeslib.as_array(a.weights, shape=(27,))
+    assert np.array_equal(w, k.weights.reshape(-1))
+    assert (a.src, a.dst, a.halo_lo, a.halo_hi) == (2, 1, 7, None)
+    assert (a.dims.x, a.dims.y, a.dims.z, a.kdims.x, a.address_mode) == (4, 5, 6, 3, int(vk.AddressMode.WRAP))
+    assert (a.z_offset, a.global_nz, a.out_z_begin, a.out_z_end, a.flags) == (3, 9, 1, 5, 2)
+    k.weights[1, 1, 1] = 0.25  # in place: the cached flat array is a view
+    a2, _ = make_args(1, 2, (4, 5, 6), vk.DataFormat.UINT8, (0.0, 1.0), k, vk.AddressMode.CLAMP)
+    assert np.ctypeslib.as_array(a2.weights, shape=(27,))[13] == 0.25
+    k.weights = np.full((3, 3, 3), 1.0 / 27)  # reassigned: repacked
+    a3, keep3 = make_args(1, 2, (4, 5, 6), vk.DataFormat.UINT8, (0.0, 1.0), k, vk.AddressMode.CLAMP)
+    assert np.allclose(np.ctypeslib.as_array(a3.weights, shape=(27,)), 1.0 / 27)
+    assert ctypes.addressof(a3.weights.contents) == keep3.ctypes.data

@@ -612,14 +612,18 @@ __device__ __forceinline__ uint32_t q32(float a) {
 template <>
 __device__ __forceinline__ void store4<uint16_t>(uint16_t* out, float a0, float a1, float a2,
                                                  float a3) {
-  __stcs(reinterpret_cast<uint2*>(out), make_uint2(q32<uint16_t>(a0) | (q32<uint16_t>(a1) << 16),
-                                                   q32<uint16_t>(a2) | (q32<uint16_t>(a3) << 16)));
+  // byte permutes (ALU pipe) rather than shift-or, which ptxas emits as
+  // IMAD on the FMA pipe the FFMA2 stream needs
+  __stcs(reinterpret_cast<uint2*>(out),
+         make_uint2(__byte_perm(q32<uint16_t>(a0), q32<uint16_t>(a1), 0x5410),
+                    __byte_perm(q32<uint16_t>(a2), q32<uint16_t>(a3), 0x5410)));
 }
 template <>
 __device__ __forceinline__ void store4<uint8_t>(uint8_t* out, float a0, float a1, float a2,
                                                 float a3) {
-  __stcs(reinterpret_cast<unsigned int*>(out), q32<uint8_t>(a0) | (q32<uint8_t>(a1) << 8) |
-                                                   (q32<uint8_t>(a2) << 16) | (q32<uint8_t>(a3) << 24));
+  const uint32_t lo = __byte_perm(q32<uint8_t>(a0), q32<uint8_t>(a1), 0x0040);
+  const uint32_t hi = __byte_perm(q32<uint8_t>(a2), q32<uint8_t>(a3), 0x0040);
+  __stcs(reinterpret_cast<unsigned int*>(out), __byte_perm(lo, hi, 0x5410));
 }
 
 // Rolling accumulators of one thread: slot m holds the partial sums of the

@@ -13,7 +13,7 @@ from __future__ import annotations
 from . import _capi
 from .execution import timed
 from .geom import clip_box, coerce_box
-from .volume import StructuredVolume, quantize_scalar, stored_bits
+from .volume import StructuredVolume, fill_bits
 
 
 @timed("FillRange")
@@ -24,7 +24,7 @@ def fill_range(volume: StructuredVolume, roi, value: float) -> None:
     box = clip_box(coerce_box(roi), volume.bounds)
     if box.is_empty:
         return
-    bits = stored_bits(quantize_scalar(value, volume.format, volume.mapping), volume.format)
+    bits = fill_bits(value, volume.format, volume.mapping)
     stream = torch.cuda.current_stream(volume.data.device)
     _capi.check(_capi.load().vkt_fill_box(
         volume.data_ptr(), _capi.int3(volume.dims), volume.format.value,

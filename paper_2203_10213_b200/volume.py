@@ -16,6 +16,8 @@ import math
 from enum import Enum
 from typing import Optional
 
+import struct
+
 import numpy as np
 
 from .errors import AllocationFailure, DeviceFailure, IndexOutOfRange, InvalidArgument
@@ -127,6 +129,31 @@ def dequantize_scalar(stored, fmt: DataFormat, mapping: VoxelMapping) -> float:
     if fmt is DataFormat.FLOAT32:
         return float(s)
     return float(mapping.lo + (s / fmt.max_int) * (mapping.hi - mapping.lo))
+
+
+def fill_bits(value: float, fmt: DataFormat, mapping: VoxelMapping) -> int:
+    """``stored_bits(quantize_scalar(value, ...))`` without numpy scalars.
+
+    Python floats are IEEE float64, so ``(v - lo) / (hi - lo)``, the clip,
+    ``t * max + 0.5`` and ``floor`` round exactly as the numpy sequence of
+    volume.py:102-110 does; float32 rounding goes through ``struct`` (round to
+    nearest even, as ``np.float32``).  Non-finite inputs and float32
+    overflow take the numpy path.  (The numpy scalar path cost ~15 us per
+    FillRange call.)
+    """
+    v = float(value)
+    if v - v == 0.0:  # finite
+        if fmt is DataFormat.FLOAT32:
+            try:
+                return struct.unpack("<I", struct.pack("<f", v))[0]
+            except OverflowError:
+                pass
+        else:
+            lo, hi = float(mapping.lo), float(mapping.hi)
+            t = (v - lo) / (hi - lo)
+            t = 0.0 if t < 0.0 else (1.0 if t > 1.0 else t)
+            return int(math.floor(t * fmt.max_int + 0.5))
+    return stored_bits(quantize_scalar(value, fmt, mapping), fmt)
 
 
 def stored_bits(value, fmt: DataFormat) -> int:
@@ -354,5 +381,5 @@ def require_same_layout(a: StructuredVolume, b: StructuredVolume) -> None:
 
 __all__ = [
     "DataFormat", "VoxelMapping", "StructuredVolume", "DeviceBuffer", "create_structured_volume",
-    "quantize_scalar", "dequantize_scalar", "stored_bits", "require_same_layout",
+    "quantize_scalar", "dequantize_scalar", "stored_bits", "fill_bits", "require_same_layout",
 ]

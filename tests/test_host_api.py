@@ -159,3 +159,23 @@ def test_make_args_weight_cache_follows_the_kernel():
     a3, keep3 = make_args(1, 2, (4, 5, 6), vk.DataFormat.UINT8, (0.0, 1.0), k, vk.AddressMode.CLAMP)
     assert np.allclose(np.ctypeslib.as_array(a3.weights, shape=(27,)), 1.0 / 27)
     assert ctypes.addressof(a3.weights.contents) == keep3.ctypes.data
+
+
+def test_fill_bits_matches_the_numpy_quantize_rule():
+    """fill_bits (plain float64 arithmetic) == stored_bits(quantize_scalar(...))
+    (the numpy restatement of volume.py:102-110) on edge and random values."""
+    import numpy as np
+
+    from paper_2203_10213_b200.volume import (DataFormat, VoxelMapping, fill_bits, quantize_scalar,
+                                              stored_bits)
+
+    rng = np.random.default_rng(3)
+    vals = list(rng.normal(0.5, 1.0, 3000)) + [k / 255 for k in range(256)] + \
+        [(k + 0.5) / 255 for k in range(255)] + [k / 65535 for k in range(0, 65536, 97)] + \
+        [0.0, -0.0, 1.0, 1e300, -1e300, 3.4e38, float("inf"), -float("inf")]
+    for fmt in (DataFormat.UINT8, DataFormat.UINT16, DataFormat.FLOAT32):
+        for m in (VoxelMapping(0.0, 1.0), VoxelMapping(-1.0, 3.0), VoxelMapping(0.1, 0.7)):
+            for v in vals:
+                with np.errstate(over="ignore"):
+                    want = stored_bits(quantize_scalar(v, fmt, m), fmt)
+                assert fill_bits(v, fmt, m) == want, (fmt, m, v)

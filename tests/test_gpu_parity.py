@@ -204,3 +204,23 @@ def test_fill_unaligned_boxes_all_formats():
             vk.fill_range(v, (lo, hi), 0.3)
             want = O.fill_range(base, fmt, lo, hi, 0.3)
             assert v.data.to_bytes() == want.tobytes()
+
+
+def test_fill_boxes_on_16_byte_rows_all_formats():
+    """Rows that are 16-byte multiples take the flattened short-segment fill
+    (fill_segs_kernel): every head / vector / tail split of the box rows."""
+    rng = np.random.default_rng(5)
+    for fmt, nx in ((1, 64), (2, 40), (3, 20)):
+        dims = (nx, 13, 6)
+        for lx in range(0, 17):
+            for w in (1, 3, 5, 16, 17, 23, nx - lx):
+                hx = min(nx, lx + w)
+                if hx <= lx or (lx == 0 and hx == nx):
+                    continue
+                lo, hi = (lx, 2, 1), (hx, 11, 5)
+                base = (rng.random(dims[::-1], dtype=np.float32) if fmt == 3 else
+                        rng.integers(0, 200, size=dims[::-1]).astype(O.DTYPE[fmt]))
+                v = vk.StructuredVolume.from_numpy(base, FMT[fmt])
+                vk.fill_range(v, (lo, hi), 0.7)
+                want = O.fill_range(base, fmt, lo, hi, 0.7)
+                assert v.data.to_bytes() == want.tobytes(), (fmt, lo, hi)

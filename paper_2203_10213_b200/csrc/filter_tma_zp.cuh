@@ -390,7 +390,10 @@ struct FixList {
 // gather in fixup_f32 stalled every plane of every edge tile).
 template <int R>
 struct WrapList {
-  static constexpr int NB = 6;
+  // 5 per lane covers a K = 3 window (one halo row of 130 cells plus 5 side
+  // cells); at 4 CTAs/SM (128 registers) the list still spilled (1.76 vs
+  // 1.55 ms), so Wrap keeps 3 CTAs/SM
+  static constexpr int NB = 5;
   int dst[NB], off[NB];
   float val[NB];
   bool ok = false;

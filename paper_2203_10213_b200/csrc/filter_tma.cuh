@@ -552,13 +552,120 @@ __device__ __forceinline__ void apply_repair_table(float* rdy, const T* raw, con
   }
 }
 
+// Wrap at K >= 5 patches its cells from a WrapList after the main pass; the
+// other repairing modes (and Wrap at K = 3) leave edge items to the repair
+// pass.
+template <int MODE, int K>
+constexpr bool kRepairs = MODE != VKT_BORDER && !(MODE == VKT_WRAP && K >= 5);
+
+// Wrap, K >= 5: the out-of-volume cells of the read window take their values
+// from the far faces of the plane, in global memory, at offsets fixed for the
+// CTA.  Each staging thread holds up to NB of them -- the global offset in
+// the plane, the (one or two: cells x0+60..x0+67 sit in a low and a high
+// pair) ready-stage float offsets packed as 16-bit halves -- and gathers the
+// values for the plane its warp half stages NEXT while this one is staged,
+// so the global round trip is off the staging critical path.  (Per item and
+// per plane, the gathers stalled every staging warp of an edge tile: cfg5
+// Wrap ran 25% behind Clamp.)  The main staging pass writes TMA's zero fill
+// for these cells; a half-wide named barrier orders the patch after it.
+template <typename T, int K, int NT>
+struct WrapList {
+  using C = Cfg<T, K>;
+  static constexpr int R = C::R;
+  static constexpr int NB = 4;
+  int off[NB];
+  uint32_t dst[NB];  // lo: first ready offset, hi: second (0xFFFF: none); 0xFFFFFFFF: no entry
+  float val[NB];
+  bool overflow;     // more than NB * NT cells (volumes thinner than TY + R)
+
+  // Cell q of the window [x0-R, min(x0+TX,nx)+R) x [y0-R, min(y0+TY,ny)+R):
+  // rows above / below the volume in full, then the left / right strips of
+  // the other rows.  Returns the cell count.
+  __device__ __forceinline__ static int cell(const TmaParams& p, int x0, int y0, int q, int& gx,
+                                             int& gy) {
+    const int xa = x0 - R, xb = min(x0 + TX, p.nx) + R;
+    const int ya = y0 - R, yb = min(y0 + TY, p.ny) + R;
+    const int w = xb - xa, rows = yb - ya;
+    const int top = min(rows, max(0, -ya));
+    const int bot = min(rows - top, max(0, yb - p.ny));
+    const int nl = max(0, -xa);
+    const int side = nl + max(0, xb - p.nx);
+    const int n_rows = (top + bot) * w;
+    if (q < n_rows) {
+      const int r = q / w;
+      gy = r < top ? ya + r : p.ny + (r - top);
+      gx = xa + (q - r * w);
+    } else if (side > 0) {
+      const int q2 = q - n_rows;
+      const int r = q2 / side;
+      const int c = q2 - r * side;
+      gy = ya + top + r;
+      gx = c < nl ? xa + c : p.nx + (c - nl);
+    }
+    return n_rows + (rows - top - bot) * side;
+  }
+  // ready-stage offsets of cell (gx, gy), packed as above
+  __device__ __forceinline__ static uint32_t dests(int x0, int y0, int gx, int gy) {
+    const int by = gy - y0 + R, e = gx - x0 + 4;  // ready row, cell column
+    const uint32_t d0 = e < NPR ? (uint32_t)(by * C::RPF + 2 * e) : 0xFFFFu;
+    const uint32_t d1 = e >= HALF ? (uint32_t)(by * C::RPF + 2 * (e - HALF) + 1) : 0xFFFFu;
+    return d0 != 0xFFFFu ? (d0 | (d1 << 16)) : (d1 | 0xFFFF0000u);
+  }
+  __device__ __forceinline__ static void put(float* rdy, uint32_t d, float v) {
+    rdy[d & 0xFFFFu] = v;
+    if ((d >> 16) != 0xFFFFu) rdy[d >> 16] = v;
+  }
+
+  __device__ __forceinline__ WrapList(const TmaParams& p, int x0, int y0, bool active, int t) {
+    int gx = 0, gy = 0;
+    const int total = active ? cell(p, x0, y0, 0, gx, gy) : 0;
+    overflow = total > NB * NT;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int q = t + NT * b;
+      dst[b] = 0xFFFFFFFFu;
+      off[b] = 0;
+      val[b] = 0.f;
+      if (q < total) {
+        cell(p, x0, y0, q, gx, gy);
+        off[b] = map_index32<VKT_WRAP>(gy, p.ny) * p.pitch + map_index32<VKT_WRAP>(gx, p.nx);
+        dst[b] = dests(x0, y0, gx, gy);
+      }
+    }
+  }
+  __device__ __forceinline__ void gather(const T* plane) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (dst[b] != 0xFFFFFFFFu) val[b] = widen(__ldg(plane + off[b]));
+  }
+  // plane: this stage's source plane, for the cells past the list (rare)
+  __device__ __forceinline__ void apply(float* rdy, const T* plane, const TmaParams& p, int x0,
+                                        int y0, int t) const {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (dst[b] != 0xFFFFFFFFu) put(rdy, dst[b], val[b]);
+    if (overflow) {
+      int gx = 0, gy = 0;
+      const int total = cell(p, x0, y0, 0, gx, gy);
+#pragma unroll 1
+      for (int q = t + NB * NT; q < total; q += NT) {
+        cell(p, x0, y0, q, gx, gy);
+        const float v = widen(__ldg(plane + map_index32<VKT_WRAP>(gy, p.ny) * p.pitch +
+                                    map_index32<VKT_WRAP>(gx, p.nx)));
+        put(rdy, dests(x0, y0, gx, gy), v);
+      }
+    }
+  }
+};
+static_assert(Cfg<float, 7>::RPF * Cfg<float, 7>::BY < 0xFFFF, "ready offsets fit 16 bits");
+
 template <typename T, int MODE, int K, int NT>
 __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* plane,
                                             const TmaParams& p, int x0, int y0, bool edge,
-                                            const StagePlan<T, K, NT, MODE != VKT_BORDER>& sp,
+                                            const StagePlan<T, K, NT, kRepairs<MODE, K>>& sp,
                                             const RepairTable& rt, int t) {
 #pragma unroll
-  for (int k = 0; k < StagePlan<T, K, NT, MODE != VKT_BORDER>::QPT; ++k) {
+  for (int k = 0; k < StagePlan<T, K, NT, kRepairs<MODE, K>>::QPT; ++k) {
     int ro, wo;
     sp.get(k, ro, wo);
     if (ro < 0) continue;
@@ -583,7 +690,7 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
   // ptxas's allocation of the FFMA2 main loop (spills, lost uniform weights).
   if constexpr (MODE == VKT_CLAMP || MODE == VKT_MIRROR) {
     if (edge) apply_repair_table<T, K>(rdy, raw, rt, t, NT);
-  } else if constexpr (MODE == VKT_WRAP) {
+  } else if constexpr (MODE == VKT_WRAP && K < 5) {
     if (edge) {
 #pragma unroll 1
       for (int k = 0; k < StagePlan<T, K, NT, true>::QPT; ++k) {
@@ -786,7 +893,11 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   };
 
   // stage plane j (SW warps, equal shares) into ready slot j % S
-  const StagePlan<T, K, ST, MODE != VKT_BORDER> splan(p, x0, y0, edge, tid % ST);
+  const StagePlan<T, K, ST, kRepairs<MODE, K>> splan(p, x0, y0, edge, tid % ST);
+  constexpr bool WLIST = MODE == VKT_WRAP && K >= 5;
+  static_assert(!WLIST || SPLIT, "the Wrap list assumes the split staging layout");
+  WrapList<T, K, ST> wlist(p, x0, y0, WLIST && edge, tid % ST);
+  if (WLIST && edge && half < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + half)));
   auto prepare = [&](int j) {
     if (SPLIT && half != (j & 1)) return;
     const int s = j % S;
@@ -803,6 +914,14 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
 #ifndef VKT_EXP_NOCONVERT  // diagnostics builds only (build.py --variant)
       stage_plane<T, MODE, K, ST>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, edge, splan, rtab,
                                   tid % ST);
+      if constexpr (WLIST) {
+        if (edge) {
+          // after the whole half's main pass (it wrote the zero fill there)
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(ST) : "memory");
+          wlist.apply(stage, plane_ptr<T>(p, src), p, x0, y0, tid % ST);
+          if (j + 2 < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + j + 2)));
+        }
+      }
 #endif
     }
     __syncwarp();

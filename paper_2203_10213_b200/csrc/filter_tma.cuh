@@ -374,16 +374,6 @@ struct StagePlan {
       compute(k, ro, wo);
     }
   }
-  // item k of the column-major repair pass (edge tiles): the items of one
-  // ready column are consecutive, so an edge column's repairs fall on the
-  // lanes of one warp instead of a few lanes of every warp.  Returns the
-  // ready offset, or -1 if the item has no out-of-volume cell.
-  __device__ __forceinline__ void repair_item_offset(int k, int& ro, int& wo) const {
-    const int q = t_ + k * NT;
-    const int g = q / C::BY, by = q - g * C::BY;
-    ro = q < NQ && slow(by, g) ? by * C::RPF + 8 * g : -1;
-    wo = by * C::BX + 4 * g + (C::A - 4);
-  }
 };
 
 // 4 consecutive raw cells -> 4 words: u8/u16 as the exponent-trick bit
@@ -410,55 +400,6 @@ __device__ __forceinline__ void load_quad(const T* src, uint32_t (&b)[4]) {
     b[2] = w.z;
     b[3] = w.w;
   }
-}
-
-// Out-of-volume repair of one staging item (edge tiles only), one cell at a
-// time (a rolled loop: unrolled, its eight gathers in flight inflated the
-// register allocation of the whole FFMA2 main loop into spills).
-template <typename T, int MODE, int K>
-__device__ __forceinline__ void repair_item(float* rdy, const T* raw, const T* plane,
-                                            const TmaParams* pp, int x0, int y0, int ro, int wo) {
-  using C = Cfg<T, K>;
-  constexpr int R = C::R;
-  const TmaParams& p = *pp;
-  uint32_t lo[4], hi[4];
-  load_quad<T>(raw + wo, lo);
-  load_quad<T>(raw + wo + HALF, hi);
-  float f[8];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    if constexpr (sizeof(T) == 4) {
-      f[c] = __uint_as_float(lo[c]);
-      f[c + 4] = __uint_as_float(hi[c]);
-    } else {
-      f[c] = __uint_as_float(lo[c]) - 8388608.0f;
-      f[c + 4] = __uint_as_float(hi[c]) - 8388608.0f;
-    }
-  }
-  constexpr int RPF = C::RPF;
-  const int by = ro / RPF, e = (ro - by * RPF) / 2;  // first cell column x0-4+e
-  const int gy = y0 - R + by;
-  const bool yo = gy < 0 || gy >= p.ny;
-  // rows past the read window of the valid outputs are left alone (their
-  // fold would leave the staged box)
-  const bool yin = gy < min(y0 + TY, p.ny) + R;
-  // halo cells overshoot by <= R <= 4: one fold is exact for extents >= 4
-  const bool near = p.nx >= 4 && p.ny >= 4;
-  const int my = near ? map_index_near<MODE>(gy, p.ny) : map_index32<MODE>(gy, p.ny);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int gx = x0 - 4 + e + (c & 3) + (c >> 2) * HALF;
-    if (yin && (yo || gx < 0 || gx >= p.nx) && gx >= x0 - R && gx < min(x0 + TX, p.nx) + R) {
-      const int mx = near ? map_index_near<MODE>(gx, p.nx) : map_index32<MODE>(gx, p.nx);
-      if constexpr (MODE == VKT_WRAP)
-        f[c] = widen(__ldg(plane + (int64_t)my * p.pitch + mx));
-      else
-        f[c] = widen(raw[(my - y0 + R) * C::BX + (mx - x0 + C::A)]);
-    }
-  }
-  const int so = by * RPF + Ready<K>::in_row(2 * e);
-  *reinterpret_cast<float4*>(rdy + so) = make_float4(f[0], f[4], f[1], f[5]);
-  *reinterpret_cast<float4*>(rdy + Ready<K>::second(so)) = make_float4(f[2], f[6], f[3], f[7]);
 }
 
 // The repair table: count, then per entry the 8 raw source cells (lo quad,
@@ -552,13 +493,12 @@ __device__ __forceinline__ void apply_repair_table(float* rdy, const T* raw, con
   }
 }
 
-// Wrap at K >= 5 patches its cells from a WrapList after the main pass; the
-// other repairing modes (and Wrap at K = 3) leave edge items to the repair
-// pass.
-template <int MODE, int K>
-constexpr bool kRepairs = MODE != VKT_BORDER && !(MODE == VKT_WRAP && K >= 5);
+// Clamp / Mirror leave edge items to the repair-table pass; Wrap patches its
+// cells from a WrapList after the main pass; Border needs no repair.
+template <int MODE>
+constexpr bool kRepairs = MODE == VKT_CLAMP || MODE == VKT_MIRROR;
 
-// Wrap, K >= 5: the out-of-volume cells of the read window take their values
+// Wrap: the out-of-volume cells of the read window take their values
 // from the far faces of the plane, in global memory, at offsets fixed for the
 // CTA.  Each staging thread holds up to NB of them -- the global offset in
 // the plane, the (one or two: cells x0+60..x0+67 sit in a low and a high
@@ -572,7 +512,7 @@ template <typename T, int K, int NT>
 struct WrapList {
   using C = Cfg<T, K>;
   static constexpr int R = C::R;
-  static constexpr int NB = 4;
+  static constexpr int NB = K == 3 ? 2 : 4;
   int off[NB];
   uint32_t dst[NB];  // lo: first ready offset, hi: second (0xFFFF: none); 0xFFFFFFFF: no entry
   float val[NB];
@@ -607,8 +547,10 @@ struct WrapList {
   // ready-stage offsets of cell (gx, gy), packed as above
   __device__ __forceinline__ static uint32_t dests(int x0, int y0, int gx, int gy) {
     const int by = gy - y0 + R, e = gx - x0 + 4;  // ready row, cell column
-    const uint32_t d0 = e < NPR ? (uint32_t)(by * C::RPF + 2 * e) : 0xFFFFu;
-    const uint32_t d1 = e >= HALF ? (uint32_t)(by * C::RPF + 2 * (e - HALF) + 1) : 0xFFFFu;
+    // in-row float f of the paired layout, through the row's bank swizzle
+    auto phys = [&](int f) { return (uint32_t)(by * C::RPF + Ready<K>::in_row(f & ~3) + (f & 3)); };
+    const uint32_t d0 = e < NPR ? phys(2 * e) : 0xFFFFu;
+    const uint32_t d1 = e >= HALF ? phys(2 * (e - HALF) + 1) : 0xFFFFu;
     return d0 != 0xFFFFu ? (d0 | (d1 << 16)) : (d1 | 0xFFFF0000u);
   }
   __device__ __forceinline__ static void put(float* rdy, uint32_t d, float v) {
@@ -662,10 +604,10 @@ static_assert(Cfg<float, 7>::RPF * Cfg<float, 7>::BY < 0xFFFF, "ready offsets fi
 template <typename T, int MODE, int K, int NT>
 __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* plane,
                                             const TmaParams& p, int x0, int y0, bool edge,
-                                            const StagePlan<T, K, NT, kRepairs<MODE, K>>& sp,
+                                            const StagePlan<T, K, NT, kRepairs<MODE>>& sp,
                                             const RepairTable& rt, int t) {
 #pragma unroll
-  for (int k = 0; k < StagePlan<T, K, NT, kRepairs<MODE, K>>::QPT; ++k) {
+  for (int k = 0; k < StagePlan<T, K, NT, kRepairs<MODE>>::QPT; ++k) {
     int ro, wo;
     sp.get(k, ro, wo);
     if (ro < 0) continue;
@@ -685,20 +627,11 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
     *reinterpret_cast<uint4*>(rdy + Ready<K>::second(ro)) =
         make_uint4((uint32_t)pr[2], (uint32_t)(pr[2] >> 32), (uint32_t)pr[3], (uint32_t)(pr[3] >> 32));
   }
-  // Clamp / Mirror: from the CTA's repair table; Wrap (global sources): cell
-  // by cell.  One mechanism per kernel: each extra repair path changed
-  // ptxas's allocation of the FFMA2 main loop (spills, lost uniform weights).
+  // Clamp / Mirror: from the CTA's repair table (Wrap: WrapList, after the
+  // pass).  One mechanism per kernel: each extra repair path changed ptxas's
+  // allocation of the FFMA2 main loop (spills, lost uniform weights).
   if constexpr (MODE == VKT_CLAMP || MODE == VKT_MIRROR) {
     if (edge) apply_repair_table<T, K>(rdy, raw, rt, t, NT);
-  } else if constexpr (MODE == VKT_WRAP && K < 5) {
-    if (edge) {
-#pragma unroll 1
-      for (int k = 0; k < StagePlan<T, K, NT, true>::QPT; ++k) {
-        int ro, wo;
-        sp.repair_item_offset(k, ro, wo);
-        if (ro >= 0) repair_item<T, MODE, K>(rdy, raw, plane, &p, x0, y0, ro, wo);
-      }
-    }
   }
 }
 
@@ -893,11 +826,12 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   };
 
   // stage plane j (SW warps, equal shares) into ready slot j % S
-  const StagePlan<T, K, ST, kRepairs<MODE, K>> splan(p, x0, y0, edge, tid % ST);
-  constexpr bool WLIST = MODE == VKT_WRAP && K >= 5;
-  static_assert(!WLIST || SPLIT, "the Wrap list assumes the split staging layout");
+  const StagePlan<T, K, ST, kRepairs<MODE>> splan(p, x0, y0, edge, tid % ST);
+  constexpr bool WLIST = MODE == VKT_WRAP;
+  constexpr int WSTEP = SPLIT ? 2 : 1;  // the next plane this warp half stages
   WrapList<T, K, ST> wlist(p, x0, y0, WLIST && edge, tid % ST);
-  if (WLIST && edge && half < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + half)));
+  if (WLIST && edge && (SPLIT ? half : 0) < np)
+    wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + (SPLIT ? half : 0))));
   auto prepare = [&](int j) {
     if (SPLIT && half != (j & 1)) return;
     const int s = j % S;
@@ -919,7 +853,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
           // after the whole half's main pass (it wrote the zero fill there)
           asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(ST) : "memory");
           wlist.apply(stage, plane_ptr<T>(p, src), p, x0, y0, tid % ST);
-          if (j + 2 < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + j + 2)));
+          if (j + WSTEP < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + j + WSTEP)));
         }
       }
 #endif

@@ -352,6 +352,14 @@ def run_ours(args):
             roof["traffic"] = ent["total_bytes"]
             roof["traffic_note"] = (f"dram read+write per launch from {ent['capture']} "
                                     f"(algorithmic {ent['algorithmic_bytes']} B)")
+    # ncu-measured achieved DRAM GB/s (3^3) and FMA-pipe utilisation (7^3) of
+    # the north-star kernels, from the committed captures (a number taken
+    # under ncu is never a bench value; these explain the CUDA-event rates)
+    ncu_ns = None
+    if tf.exists():
+        ncu_ns = json.loads(tf.read_text()).get("north_star_ncu")
+        if ncu_ns:
+            ncu_ns = dict(ncu_ns, peaks={"hbm_gbs": hbm_gbs, "fma_pipe_pct": 100.0})
 
     extra = None
     if world == 1 and not args.no_extra:
@@ -388,6 +396,7 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "north_star_f32_1024": extra,
+            "ncu": ncu_ns,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

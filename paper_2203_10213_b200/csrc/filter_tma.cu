@@ -80,7 +80,7 @@ bool tma_supported(const vkt_filter_args& a) {
   if (a.flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
   const int k = a.kdims.x;
   if (a.kdims.y != k || a.kdims.z != k) return false;
-  if (k != 3 && k != 5 && k != 7) return false;
+  if (k != 3 && k != 5 && k != 7 && k != 9) return false;
 
   // rows that are not 16-byte multiples (or unaligned buffers) are staged
   // through pitched scratch copies (launch_filter_tma), so every extent works
@@ -124,7 +124,7 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
   // K = 3 (4, Wrap 3)
   const int64_t slots = 148ll * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
-                                 : k == 7 ? tma::Layout<2, 7>::CTAS_PER_SM
+                                 : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
                                           : tma::Layout<2, 3>::CTAS_PER_SM);
   int zc = 64;

@@ -141,7 +141,7 @@ struct Cfg {
   static constexpr int S_RDY_FIT = (BUDGET - VKT_RAW_MIN * RAW_PITCH) / RDY_PITCH;
   // K = 3 integer rings (4 CTAs/SM) drop to 3 ready stages with AHEAD = 1,
   // leaving room for deeper raw rings (u8 1.62 -> 1.58 ms; u16 needs it to fit)
-  static constexpr int S_RDY_MIN = L::SMALL ? 3 : 4;
+  static constexpr int S_RDY_MIN = (L::SMALL || K == 9) ? 3 : 4;  // K = 9: 24-row stages
   static constexpr int S_RDY = S_RDY_FIT < S_RDY_MIN ? S_RDY_MIN : (S_RDY_FIT > 6 ? 6 : S_RDY_FIT);
   static constexpr int S_RAW_FIT = (BUDGET - S_RDY * RDY_PITCH) / RAW_PITCH;
   static constexpr int S_RAW = S_RAW_FIT < 10 ? S_RAW_FIT : 10;
@@ -512,7 +512,7 @@ template <typename T, int K, int NT>
 struct WrapList {
   using C = Cfg<T, K>;
   static constexpr int R = C::R;
-  static constexpr int NB = K == 3 ? 2 : 4;
+  static constexpr int NB = K == 3 ? 2 : (K == 9 ? 2 : 4);  // K = 9: registers
   int off[NB];
   uint32_t dst[NB];  // lo: first ready offset, hi: second (0xFFFF: none); 0xFFFFFFFF: no entry
   float val[NB];
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     // (GUARD, 2R of every chunk's ~70) keep it rolled at K = 7, which keeps
     // the kernel's hot code compact (K = 7: 11.76 -> 11.33 ms for u16, 11.39
     // -> 11.11 ms for f32, against all-rolled / all-unrolled).
-    constexpr bool UNROLL = true;
+    constexpr bool UNROLL = K <= 7;  // K = 9 unrolled: ~2900 FFMA2 per plane body
     constexpr bool UNROLL_G = K <= 5;  // K = 5 with rolled ramps: 4.60 vs 4.46 ms
     if (first <= 0 && last >= K - 1)
       plane_step<K, YPT, false, UNROLL>(stage, ld_off, ty, wt, acc, 0, K - 1);
@@ -1002,6 +1002,7 @@ cudaError_t launch_tma_dtype(int k, int mode, const CUtensorMap& ms, const CUten
   VKT_TMA_K(3)
   VKT_TMA_K(5)
   VKT_TMA_K(7)
+  VKT_TMA_K(9)
 #undef VKT_TMA_K
 #undef VKT_TMA_CASE
   return cudaErrorInvalidValue;

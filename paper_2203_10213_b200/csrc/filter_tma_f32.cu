@@ -29,6 +29,7 @@ cudaError_t launch_tma_dtype<float>(int k, int mode, const CUtensorMap& ms, cons
     }
   VKT_F32_CASES(5)
   VKT_F32_CASES(7)
+  VKT_F32_CASES(9)
 #undef VKT_F32_CASES
   return cudaErrorInvalidValue;
 }

@@ -68,3 +68,24 @@ def test_interior_tiles_at_z_boundaries(fmt, k):
         got = _run(stored, fmt, w, mode, "auto")
         ok, ndiff, dmax = within_contract(got, want, fmt)
         assert ok, (k, mode, ndiff, dmax)
+
+
+@pytest.mark.parametrize("fmt", [1, 2, 3])
+@pytest.mark.parametrize("shape", [(140, 40, 11), (33, 7, 5), (256, 20, 3)], ids=lambda s: "x".join(map(str, s)))
+def test_tiled_k9_all_modes(shape, fmt):
+    """9x9x9 runs on the tiled kernel (R = 4, the largest halo its layout
+    takes): within contract against the oracle under every address mode."""
+    rng = np.random.default_rng(900 + fmt)
+    nx, ny, nz = shape
+    stored = (rng.random((nz, ny, nx), dtype=np.float32) if fmt == 3 else
+              rng.integers(0, np.iinfo(O.DTYPE[fmt]).max + 1, size=(nz, ny, nx), dtype=O.DTYPE[fmt]))
+    w = rng.random((9, 9, 9))
+    w /= w.sum()
+    src = vk.StructuredVolume.from_numpy(stored, FMT[fmt])
+    dst = vk.StructuredVolume(src.dims, src.format)
+    assert vk.filter_path(dst, src, vk.Kernel((9, 9, 9), w.reshape(-1))) == "tma"
+    for mode in ("wrap", "mirror", "clamp", "border"):
+        want = O.apply_filter(stored, fmt, w, mode, workers=1)
+        got = _run(stored, fmt, w, mode, "auto")
+        ok, ndiff, dmax = within_contract(got, want, fmt)
+        assert ok, (shape, mode, ndiff, dmax)

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "dispatch.h"
@@ -134,6 +135,37 @@ static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
   return VKT_OK;
 }
 
+// Anisotropic integer kernels on the tiled kernel: embed the (kx, ky, kz)
+// weights centred in a K^3 cube of zeros, K = max extent.  Integer voxels
+// widen to finite non-negative floats, so every added tap contributes an
+// exact +0 and the FP32 sums -- the same nonzero products in the same
+// relative (dz, dy, dx) order -- are bit-identical to the unpadded ones.
+// (f32 volumes are not padded: a zero weight times an Inf would inject NaN.)
+// The z extent may only grow when no halo buffers are involved: halos are
+// sized for the caller's kz.
+static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vector<double>& w) {
+  if (a->flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
+  if (a->format == VKT_F32) return false;
+  const int kx = a->kdims.x, ky = a->kdims.y, kz = a->kdims.z;
+  if (kx == ky && ky == kz) return false;
+  int k = kx > ky ? kx : ky;
+  k = k > kz ? k : kz;
+  if (k != 3 && k != 5 && k != 7 && k != 9) return false;
+  const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
+                         (a->global_nz <= 0 || a->global_nz == a->dims.z);
+  if (kz != k && !unsharded) return false;
+  w.assign((size_t)k * k * k, 0.0);
+  const int ox = (k - kx) / 2, oy = (k - ky) / 2, oz = (k - kz) / 2;
+  for (int z = 0; z < kz; ++z)
+    for (int y = 0; y < ky; ++y)
+      for (int x = 0; x < kx; ++x)
+        w[((size_t)(z + oz) * k + (y + oy)) * k + (x + ox)] = a->weights[((size_t)z * ky + y) * kx + x];
+  out = *a;
+  out.kdims = vkt_int3{k, k, k};
+  out.weights = w.data();
+  return true;
+}
+
 }  // namespace vkt
 
 using namespace vkt;
@@ -144,6 +176,18 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
   FilterPlan plan;
   int st = validate_and_plan(args, plan);
   if (st != VKT_OK) return st;
+  if (plan.path == VKT_PATH_DIRECT) {
+    vkt_filter_args cube;
+    std::vector<double> wcube;
+    if (pad_to_cube(args, cube, wcube)) {
+      FilterPlan p2;
+      if (validate_and_plan(&cube, p2) == VKT_OK && p2.path == VKT_PATH_TMA) {
+        if (p2.z_end <= p2.z_begin) return VKT_OK;
+        const int st2 = launch_filter_tma(p2, reinterpret_cast<cudaStream_t>(stream));
+        if (st2 != -1) return st2;
+      }
+    }
+  }
   if (plan.z_end <= plan.z_begin) return VKT_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (plan.path == VKT_PATH_TMA) {
@@ -157,6 +201,12 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
 int vkt_filter_path(const vkt_filter_args* args) {
   FilterPlan plan;
   if (validate_and_plan(args, plan) != VKT_OK) return VKT_PATH_NONE;
+  if (plan.path == VKT_PATH_DIRECT) {
+    vkt_filter_args cube;
+    std::vector<double> wcube;
+    FilterPlan p2;
+    if (pad_to_cube(args, cube, wcube) && validate_and_plan(&cube, p2) == VKT_OK) return p2.path;
+  }
   return plan.path;
 }
 

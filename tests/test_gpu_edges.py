@@ -89,3 +89,35 @@ def test_tiled_k9_all_modes(shape, fmt):
         got = _run(stored, fmt, w, mode, "auto")
         ok, ndiff, dmax = within_contract(got, want, fmt)
         assert ok, (shape, mode, ndiff, dmax)
+
+
+@pytest.mark.parametrize("fmt", [1, 2])
+@pytest.mark.parametrize("kd", [(3, 1, 5), (5, 5, 1), (1, 3, 3), (7, 3, 1), (9, 1, 1), (3, 3, 5)],
+                         ids=lambda k: "x".join(map(str, k)))
+def test_anisotropic_integer_kernels_on_the_tiled_path(kd, fmt):
+    """Anisotropic integer kernels run on the tiled kernel, embedded in a K^3
+    cube of zero weights: bit-identical to the direct kernel (same FP32 tap
+    sequence; the zero taps add exact +0) and within contract of the oracle."""
+    rng = np.random.default_rng(77 + fmt)
+    stored = rng.integers(0, np.iinfo(O.DTYPE[fmt]).max + 1, size=(7, 21, 140), dtype=O.DTYPE[fmt])
+    w = rng.random(kd[::-1])
+    w /= w.sum()
+    src = vk.StructuredVolume.from_numpy(stored, FMT[fmt])
+    dst = vk.StructuredVolume(src.dims, src.format)
+    assert vk.filter_path(dst, src, vk.Kernel(kd, w.reshape(-1))) == "tma"
+    kernel = vk.Kernel(kd, w.reshape(-1))
+
+    def run(mode, path):
+        vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
+        try:
+            vk.ApplyFilter(dst, src, kernel, mode)
+            return dst.to_numpy()
+        finally:
+            vk.set_execution_policy(vk.ExecutionPolicy())
+
+    for mode in ("wrap", "mirror", "clamp", "border"):
+        want = O.apply_filter(stored, fmt, w, mode, workers=1)
+        got = run(mode, "auto")
+        ok, ndiff, dmax = within_contract(got, want, fmt)
+        assert ok, (kd, mode, ndiff, dmax)
+        assert np.array_equal(got, run(mode, "direct")), (kd, mode)

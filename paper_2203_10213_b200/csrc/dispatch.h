@@ -18,6 +18,7 @@ struct FilterPlan {
   double sum_w;             // f64 sum of weights (epilogue)
   float epi_c;              // lo*(sum_w-1)/(hi-lo)*max  (ints), 0 for f32
   int path;                 // VKT_PATH_*
+  uint32_t zskip = 0;       // f32 weights padded in z to a cube: bit dz = padding plane
 };
 
 void set_error_detail(const char* fmt, ...);

@@ -174,6 +174,7 @@ struct TmaParams {
   int zc;                // output planes per CTA chunk
   int64_t z_offset, global_nz;
   float c;               // integer epilogue constant
+  uint32_t zskip;        // f32 kernels padded in z: bit dz set = that dz plane is padding
 };
 
 // ---------------------------------------------------------------------------
@@ -695,11 +696,11 @@ struct LoadRun {
 // One input plane's contribution to the K rolling accumulators of the
 // thread's YPT x 4 output pairs.  GUARD: skip slots whose output plane is
 // outside the chunk (ramp up / down; those sums are never stored).
-template <int K, int YPT, bool GUARD, bool UNROLL>
+template <int K, int YPT, bool GUARD, bool UNROLL, bool ZSKIP>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
                                            const int (&off)[LoadRun<K>::NOFF], int ty,
                                            const Weights<K>& wt, Accum<K, YPT>& acc, int first,
-                                           int last) {
+                                           int last, uint32_t zskip) {
   constexpr int SH = LoadRun<K>::SH;
   constexpr int NLD = LoadRun<K>::NLD;
   constexpr int RPF = Ready<K>::RPF;
@@ -728,6 +729,9 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
     for (int m = 0; m < K; ++m) {
       if (GUARD && (m < first || m > last)) continue;
       const int dz = K - 1 - m;
+      // z planes that only pad an f32 kernel to a cube: no FMA at all (a
+      // zero weight times an Inf would inject NaN)
+      if (ZSKIP && ((zskip >> dz) & 1u)) continue;
       const float* w = wt.w + (dz * K + dy) * Weights<K>::KP;
 #pragma unroll
       for (int dx = 0; dx < K; ++dx) {
@@ -741,7 +745,7 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
   }
 }
 
-template <typename T, int K, int MODE>
+template <typename T, int K, int MODE, bool ZSKIP = false>
 __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
                                   Layout<(int)sizeof(T), K>::CTAS_PER_SM)
     filter_tma_kernel(const __grid_constant__ CUtensorMap map_src,
@@ -934,9 +938,9 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     constexpr bool UNROLL = K <= 7;  // K = 9 unrolled: ~2900 FFMA2 per plane body
     constexpr bool UNROLL_G = K <= 5;  // K = 5 with rolled ramps: 4.60 vs 4.46 ms
     if (first <= 0 && last >= K - 1)
-      plane_step<K, YPT, false, UNROLL>(stage, ld_off, ty, wt, acc, 0, K - 1);
+      plane_step<K, YPT, false, UNROLL, ZSKIP>(stage, ld_off, ty, wt, acc, 0, K - 1, p.zskip);
     else
-      plane_step<K, YPT, true, UNROLL_G>(stage, ld_off, ty, wt, acc, first, last);
+      plane_step<K, YPT, true, UNROLL_G, ZSKIP>(stage, ld_off, ty, wt, acc, first, last, p.zskip);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
@@ -963,14 +967,14 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   }
 }
 
-template <typename T, int K, int MODE>
+template <typename T, int K, int MODE, bool ZSKIP = false>
 cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, const CUtensorMap& mh,
                               const TmaParams& p, const float* w32, dim3 grid, cudaStream_t s) {
   using C = Cfg<T, K>;
   Weights<K> wt = {};
   for (int r = 0; r < K * K; ++r)
     for (int x = 0; x < K; ++x) wt.w[r * Weights<K>::KP + x] = w32[r * K + x];
-  auto fn = filter_tma_kernel<T, K, MODE>;
+  auto fn = filter_tma_kernel<T, K, MODE, ZSKIP>;
   // the shared-memory opt-in once per device (a per-call attribute set was a
   // measurable share of the host time of small launches)
   static std::atomic<uint64_t> opted{0};

@@ -147,6 +147,7 @@ struct TmaParams {
   int zc;
   int64_t z_offset, global_nz;
   float c;
+  uint32_t zskip;
 };
 
 // ---------------------------------------------------------------------------

@@ -140,17 +140,21 @@ static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
 // widen to finite non-negative floats, so every added tap contributes an
 // exact +0 and the FP32 sums -- the same nonzero products in the same
 // relative (dz, dy, dx) order -- are bit-identical to the unpadded ones.
-// (f32 volumes are not padded: a zero weight times an Inf would inject NaN.)
+// f32 volumes are padded only in z, and the kernel skips the padding planes
+// outright (a zero weight times an Inf would inject NaN).
 // The z extent may only grow when no halo buffers are involved: halos are
 // sized for the caller's kz.
-static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vector<double>& w) {
+static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vector<double>& w,
+                        uint32_t& zskip) {
   if (a->flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
-  if (a->format == VKT_F32) return false;
   const int kx = a->kdims.x, ky = a->kdims.y, kz = a->kdims.z;
   if (kx == ky && ky == kz) return false;
   int k = kx > ky ? kx : ky;
   k = k > kz ? k : kz;
   if (k != 3 && k != 5 && k != 7 && k != 9) return false;
+  // f32: only z padding, whose planes the kernel skips outright (no FMA, so
+  // no 0 * Inf); K = 3 f32 runs the direct-staging kernel, which cannot skip
+  if (a->format == VKT_F32 && (kx != k || ky != k || k == 3)) return false;
   const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
                          (a->global_nz <= 0 || a->global_nz == a->dims.z);
   if (kz != k && !unsharded) return false;
@@ -163,6 +167,10 @@ static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vec
   out = *a;
   out.kdims = vkt_int3{k, k, k};
   out.weights = w.data();
+  zskip = 0;
+  if (a->format == VKT_F32)
+    for (int z = 0; z < k; ++z)
+      if (z < oz || z >= oz + kz) zskip |= 1u << z;
   return true;
 }
 
@@ -179,9 +187,11 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;
-    if (pad_to_cube(args, cube, wcube)) {
+    uint32_t zskip = 0;
+    if (pad_to_cube(args, cube, wcube, zskip)) {
       FilterPlan p2;
       if (validate_and_plan(&cube, p2) == VKT_OK && p2.path == VKT_PATH_TMA) {
+        p2.zskip = zskip;
         if (p2.z_end <= p2.z_begin) return VKT_OK;
         const int st2 = launch_filter_tma(p2, reinterpret_cast<cudaStream_t>(stream));
         if (st2 != -1) return st2;
@@ -205,7 +215,8 @@ int vkt_filter_path(const vkt_filter_args* args) {
     vkt_filter_args cube;
     std::vector<double> wcube;
     FilterPlan p2;
-    if (pad_to_cube(args, cube, wcube) && validate_and_plan(&cube, p2) == VKT_OK) return p2.path;
+    uint32_t zskip = 0;
+    if (pad_to_cube(args, cube, wcube, zskip) && validate_and_plan(&cube, p2) == VKT_OK) return p2.path;
   }
   return plan.path;
 }

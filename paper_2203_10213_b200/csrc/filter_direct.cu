@@ -5,8 +5,9 @@
 // order (pkg/src/vkt/ops/filters.py:89-92) so the f32 result is bit-identical
 // to the tiled TMA kernel (filter_tma.cu) and independent of any slab split.
 // Reuse of neighbouring inputs comes from L1/L2; this kernel is the fallback
-// for shapes the tiled kernel does not specialise (anisotropic or k > 7,
-// strides that are not 16-byte multiples) and the EXACT_F64 parity mode.
+// for shapes the tiled kernel does not specialise (k > 9, k = 1, f32 kernels
+// with kx != ky -- vkt_capi.cu pads the other anisotropic ones to a cube --
+// and the EXACT_F64 parity mode.
 #include "common.cuh"
 #include "dispatch.h"
 

@@ -1,4 +1,4 @@
-// filter_tma_f32.cu — the tiled TMA kernels for float voxels (K in {3,5,7} x
+// filter_tma_f32.cu — the tiled TMA kernels for float voxels (K in {3,5,7,9} x
 // the four address modes): K = 5, 7 on the paired-layout kernel
 // (filter_tma.cuh), K = 3 on the direct-staging variant (filter_tma_zp.cuh,
 // see its header).

@@ -1,5 +1,5 @@
 // filter_tma_u8.cu — instantiates the tiled TMA kernels for uint8_t voxels
-// (K in {3,5,7} x the four address modes); see filter_tma.cuh.
+// (K in {3,5,7,9} x the four address modes); see filter_tma.cuh.
 #include "filter_tma.cuh"
 
 namespace vkt {

@@ -1,7 +1,7 @@
 """GPU: seeded random sweep of ApplyFilter against the CPU oracle.
 
 Random extents (1..70 per axis, odd and 16-byte-aligned rows), kernel shapes
-(isotropic 3/5/7 -> tiled TMA kernel, anisotropic / 1 / 9 -> direct kernel),
+(isotropic 3/5/7/9 and padded anisotropic -> tiled TMA kernel, others -> direct),
 weights (Gaussian, box, signed random), formats, mappings and all four
 address modes.  Every case checks
   * the fast path against the oracle within the BASELINE.md contract,

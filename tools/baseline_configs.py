@@ -56,6 +56,22 @@ def filt(name, n, fmt, kernel, mode, reps=20):
            "path": vk.filter_path(dst, src, kernel, mode), "ms_best": round(best, 4),
            "ms_median": round(med, 4), "gvox_s": round(nvox / best / 1e6, 2),
            "roofline": roof(nvox, fmt.bytes_per_cell, kernel.tap_count, best)}
+    if n <= 512:
+        # small volumes: also the launch replayed from a CUDA graph (device time
+        # without the ~15 us of per-call host work)
+        st = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(st)
+        with torch.cuda.stream(side):
+            vk.ApplyFilter(dst, src, kernel, mode)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(10):
+                    vk.ApplyFilter(dst, src, kernel, mode)
+        st.wait_stream(side)
+        gb, _ = timeit(g.replay, reps)
+        out["graph_ms_per_call"] = round(gb / 10, 4)
+        out["graph_roofline"] = roof(nvox, fmt.bytes_per_cell, kernel.tap_count, gb / 10)
     del src, dst
     torch.cuda.empty_cache()
     return out

@@ -63,13 +63,22 @@ def _unsharded(host, fmt, kernel, mode, path="auto"):
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("mode", list(vk.AddressMode))
 @pytest.mark.parametrize("fmt,k", [(vk.DataFormat.UINT16, 7), (vk.DataFormat.FLOAT32, 3),
-                                   (vk.DataFormat.UINT8, 5)])
+                                   (vk.DataFormat.UINT8, 5), (vk.DataFormat.FLOAT32, 9),
+                                   (vk.DataFormat.UINT8, (3, 1, 5)), (vk.DataFormat.FLOAT32, (5, 5, 1))],
+                         ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
 def test_sharded_bit_identical_to_unsharded(world, mode, fmt, k):
-    rng = np.random.default_rng(world * 100 + k)
+    # K = 9 (rz = 4 > a slab at world 8), and anisotropic kernels: (3,1,5) is
+    # cube-padded in the shards too (kz = K); (5,5,1) is padded unsharded only
+    # (no halo planes to grow into) and still matches bit for bit
+    rng = np.random.default_rng(world * 100 + (k if isinstance(k, int) else sum(k)))
     shape = (40, 24, 64)  # (z, y, x): TMA-eligible rows for every format
     host = (rng.random(shape, dtype=np.float32) if fmt is vk.DataFormat.FLOAT32 else
             rng.integers(0, np.iinfo(fmt.dtype).max + 1, size=shape, dtype=fmt.dtype))
-    kern = vk.gaussian_kernel(1.0, k) if k != 5 else vk.box_kernel(5)
+    if isinstance(k, tuple):
+        w = rng.random(k[0] * k[1] * k[2])
+        kern = vk.Kernel(k, w / w.sum())
+    else:
+        kern = vk.gaussian_kernel(1.0, k) if k != 5 else vk.box_kernel(5)
     want = _unsharded(host, fmt, kern, mode)
     got = _sharded_run(host, fmt, kern, mode, world)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))

@@ -19,6 +19,9 @@ struct FilterPlan {
   float epi_c;              // lo*(sum_w-1)/(hi-lo)*max  (ints), 0 for f32
   int path;                 // VKT_PATH_*
   uint32_t zskip = 0;       // f32 weights padded in z to a cube: bit dz = padding plane
+  // Device flag set by launch_scan_nonfinite.  Tiled launches do nothing when
+  // it is set, direct launches only then; nullptr = unconditional.
+  const int* guard = nullptr;
 };
 
 void set_error_detail(const char* fmt, ...);
@@ -30,6 +33,9 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 cudaError_t scratch_free(void* p, cudaStream_t s);
 
 int launch_filter_direct(const FilterPlan& plan, cudaStream_t s);
+// Sets *flag (device int, zeroed here) to 1 when any of the n floats at v is
+// Inf or NaN.
+int launch_scan_nonfinite(const float* v, int64_t n, int* flag, cudaStream_t s);
 // Returns VKT_OK, an error, or -1 when the tiled kernel does not cover `plan`.
 int launch_filter_tma(const FilterPlan& plan, cudaStream_t s);
 bool tma_supported(const vkt_filter_args& a);

@@ -5,9 +5,10 @@
 // order (pkg/src/vkt/ops/filters.py:89-92) so the f32 result is bit-identical
 // to the tiled TMA kernel (filter_tma.cu) and independent of any slab split.
 // Reuse of neighbouring inputs comes from L1/L2; this kernel is the fallback
-// for shapes the tiled kernel does not specialise (k > 9, k = 1, f32 kernels
-// with kx != ky -- vkt_capi.cu pads the other anisotropic ones to a cube --
-// and the EXACT_F64 parity mode.
+// for shapes the tiled kernel does not specialise (k > 9, k = 1, sharded f32
+// kernels needing x/y padding, f32 volumes with Inf/NaN under the guarded cube
+// path -- vkt_capi.cu pads the other anisotropic ones to a cube) and the
+// EXACT_F64 parity mode.
 #include "common.cuh"
 #include "dispatch.h"
 
@@ -24,10 +25,12 @@ struct DirectParams {
   const double* w64;  // device, kx*ky*kz (EXACT only)
   float c;            // fast epilogue constant (ints)
   double lo, hi, span;  // mapping (EXACT only); span = hi - lo
+  const int* run_if;   // non-null: the launch does nothing unless *run_if != 0
 };
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256) filter_direct_kernel(DirectParams p) {
+  if (p.run_if != nullptr && *p.run_if == 0) return;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= p.nx || y >= p.ny) return;
@@ -168,6 +171,7 @@ int launch_filter_direct(const FilterPlan& plan, cudaStream_t s) {
   p.lo = a.map_lo;
   p.hi = a.map_hi;
   p.span = a.map_hi - a.map_lo;
+  p.run_if = plan.guard;
 
   switch (a.format) {
     case VKT_U8: err = launch_direct_mode<uint8_t>(p, a.address_mode, exact, s); break;
@@ -177,6 +181,50 @@ int launch_filter_direct(const FilterPlan& plan, cudaStream_t s) {
   scratch_free(dw, s);
   if (err != cudaSuccess) {
     set_error_detail("filter_direct launch: %s", cudaGetErrorString(err));
+    return VKT_DEVICE_FAILURE;
+  }
+  return VKT_OK;
+}
+
+// Inf/NaN scan for the guarded cube path (vkt_capi.cu): 16-byte streaming
+// loads over the aligned body, the unaligned head and tail by the first
+// threads; one store per block that saw a non-finite value.
+__device__ __forceinline__ bool nonfinite(float v) {
+  return (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+}
+
+__global__ void __launch_bounds__(256) scan_nonfinite_kernel(const float* __restrict__ v,
+                                                             int64_t n, int64_t head, int* flag) {
+  const int64_t nvec = (n - head) / 4;
+  const float4* v4 = reinterpret_cast<const float4*>(v + head);
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (int64_t i = t0; i < nvec; i += stride) {
+    const float4 q = __ldcs(v4 + i);
+    bad |= nonfinite(q.x) | nonfinite(q.y) | nonfinite(q.z) | nonfinite(q.w);
+  }
+  const int64_t tail = head + nvec * 4;
+  if (t0 < head) bad |= nonfinite(v[t0]);
+  if (t0 < n - tail) bad |= nonfinite(v[tail + t0]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+int launch_scan_nonfinite(const float* v, int64_t n, int* flag, cudaStream_t s) {
+  cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(int), s);
+  if (err == cudaSuccess) {
+    int64_t head = (int64_t)(((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+    if (head > n) head = n;
+    const int64_t nvec = (n - head) / 4;
+    int64_t blocks = (nvec + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    scan_nonfinite_kernel<<<(unsigned)blocks, 256, 0, s>>>(v, n, head, flag);
+    count_launch();
+    err = cudaGetLastError();
+  }
+  if (err != cudaSuccess) {
+    set_error_detail("scan_nonfinite: %s", cudaGetErrorString(err));
     return VKT_DEVICE_FAILURE;
   }
   return VKT_OK;

@@ -116,6 +116,7 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   p.global_nz = plan.geom.global_nz;
   p.c = plan.epi_c;
   p.zskip = plan.zskip;
+  p.guard = plan.guard;
 
   // Chunk depth ZC: every CTA pays ~2R extra input planes plus a pipeline
   // fill; the grid pays wave quantization.  Pick the ZC with the smallest

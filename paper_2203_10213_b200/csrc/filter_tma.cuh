@@ -175,6 +175,7 @@ struct TmaParams {
   int64_t z_offset, global_nz;
   float c;               // integer epilogue constant
   uint32_t zskip;        // f32 kernels padded in z: bit dz set = that dz plane is padding
+  const int* guard;      // non-null: the launch does nothing when *guard != 0 (vkt_capi.cu)
 };
 
 // ---------------------------------------------------------------------------
@@ -752,6 +753,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
                       const __grid_constant__ CUtensorMap map_lo,
                       const __grid_constant__ CUtensorMap map_hi, const TmaParams p,
                       const __grid_constant__ Weights<K> wt) {
+  if (p.guard != nullptr && *p.guard != 0) return;  // uniform over the grid
   using C = Cfg<T, K>;
   constexpr int R = C::R;
   constexpr int S = C::S_RDY;

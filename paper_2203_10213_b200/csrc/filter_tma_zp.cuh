@@ -148,6 +148,7 @@ struct TmaParams {
   int64_t z_offset, global_nz;
   float c;
   uint32_t zskip;
+  const int* guard;
 };
 
 // ---------------------------------------------------------------------------
@@ -680,6 +681,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K, MODE>::CTAS_PER_
                       const __grid_constant__ CUtensorMap map_lo,
                       const __grid_constant__ CUtensorMap map_hi, const TmaParams p,
                       const __grid_constant__ Weights<K> wt) {
+  if (p.guard != nullptr && *p.guard != 0) return;  // uniform over the grid
   using C = Cfg<T, K, MODE>;
   constexpr int R = C::R;
   constexpr int S = C::S_RDY;

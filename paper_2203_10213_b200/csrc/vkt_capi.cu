@@ -140,23 +140,27 @@ static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
 // widen to finite non-negative floats, so every added tap contributes an
 // exact +0 and the FP32 sums -- the same nonzero products in the same
 // relative (dz, dy, dx) order -- are bit-identical to the unpadded ones.
-// f32 volumes are padded only in z, and the kernel skips the padding planes
-// outright (a zero weight times an Inf would inject NaN).
+// f32 volumes padded only in z run as they are: the kernel skips the padding
+// planes outright (a zero weight times an Inf would inject NaN).  Other f32
+// kernels (x/y padding, or K = 3, whose direct-staging kernel cannot skip)
+// are `guarded`: an Inf/NaN scan of the source picks, on the device, the
+// tiled launch when every voxel is finite (each added tap is then an exact
+// +0 again) or the direct kernel otherwise.  Unsharded volumes only (the
+// scan covers `src`, not halo buffers).
 // The z extent may only grow when no halo buffers are involved: halos are
 // sized for the caller's kz.
 static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vector<double>& w,
-                        uint32_t& zskip) {
+                        uint32_t& zskip, bool& guarded) {
   if (a->flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
   const int kx = a->kdims.x, ky = a->kdims.y, kz = a->kdims.z;
   if (kx == ky && ky == kz) return false;
   int k = kx > ky ? kx : ky;
   k = k > kz ? k : kz;
   if (k != 3 && k != 5 && k != 7 && k != 9) return false;
-  // f32: only z padding, whose planes the kernel skips outright (no FMA, so
-  // no 0 * Inf); K = 3 f32 runs the direct-staging kernel, which cannot skip
-  if (a->format == VKT_F32 && (kx != k || ky != k || k == 3)) return false;
   const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
                          (a->global_nz <= 0 || a->global_nz == a->dims.z);
+  guarded = a->format == VKT_F32 && (kx != k || ky != k || k == 3);
+  if (guarded && !unsharded) return false;
   if (kz != k && !unsharded) return false;
   w.assign((size_t)k * k * k, 0.0);
   const int ox = (k - kx) / 2, oy = (k - ky) / 2, oz = (k - kz) / 2;
@@ -168,10 +172,36 @@ static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vec
   out.kdims = vkt_int3{k, k, k};
   out.weights = w.data();
   zskip = 0;
-  if (a->format == VKT_F32)
+  if (a->format == VKT_F32 && k != 3)
     for (int z = 0; z < k; ++z)
       if (z < oz || z >= oz + kz) zskip |= 1u << z;
   return true;
+}
+
+// The guarded cube launch (see pad_to_cube): scan, tiled kernel (skipped on
+// the device when the scan found Inf/NaN), direct kernel (skipped otherwise).
+// Returns -1 when the tiled kernel does not cover the cube plan.
+static int launch_guarded(const FilterPlan& plan, FilterPlan& cube, cudaStream_t s) {
+  void* flag = nullptr;
+  cudaError_t err = scratch_alloc(&flag, sizeof(int), s);
+  if (err != cudaSuccess) {
+    set_error_detail("scratch_alloc(flag): %s", cudaGetErrorString(err));
+    return err == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
+  }
+  const vkt_filter_args& a = *plan.args;
+  int st = launch_scan_nonfinite(static_cast<const float*>(a.src),
+                                 (int64_t)a.dims.x * a.dims.y * a.dims.z, static_cast<int*>(flag), s);
+  if (st == VKT_OK) {
+    cube.guard = static_cast<const int*>(flag);
+    st = launch_filter_tma(cube, s);
+    if (st == VKT_OK) {
+      FilterPlan direct = plan;
+      direct.guard = static_cast<const int*>(flag);
+      st = launch_filter_direct(direct, s);
+    }
+  }
+  scratch_free(flag, s);
+  return st;
 }
 
 }  // namespace vkt
@@ -188,12 +218,14 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
     vkt_filter_args cube;
     std::vector<double> wcube;
     uint32_t zskip = 0;
-    if (pad_to_cube(args, cube, wcube, zskip)) {
+    bool guarded = false;
+    if (pad_to_cube(args, cube, wcube, zskip, guarded)) {
       FilterPlan p2;
       if (validate_and_plan(&cube, p2) == VKT_OK && p2.path == VKT_PATH_TMA) {
         p2.zskip = zskip;
         if (p2.z_end <= p2.z_begin) return VKT_OK;
-        const int st2 = launch_filter_tma(p2, reinterpret_cast<cudaStream_t>(stream));
+        cudaStream_t s2 = reinterpret_cast<cudaStream_t>(stream);
+        const int st2 = guarded ? launch_guarded(plan, p2, s2) : launch_filter_tma(p2, s2);
         if (st2 != -1) return st2;
       }
     }
@@ -216,7 +248,9 @@ int vkt_filter_path(const vkt_filter_args* args) {
     std::vector<double> wcube;
     FilterPlan p2;
     uint32_t zskip = 0;
-    if (pad_to_cube(args, cube, wcube, zskip) && validate_and_plan(&cube, p2) == VKT_OK) return p2.path;
+    bool guarded = false;
+    if (pad_to_cube(args, cube, wcube, zskip, guarded) && validate_and_plan(&cube, p2) == VKT_OK)
+      return p2.path;
   }
   return plan.path;
 }

@@ -156,3 +156,40 @@ def test_anisotropic_f32_z_padded_on_the_tiled_path(kd):
     vk.ApplyFilter(dst, src2, kernel, "clamp")
     ok, ndiff, dmax = within_contract(dst.to_numpy(), O.apply_filter(finite, 3, w, "clamp", workers=1), 3)
     assert ok, (kd, ndiff, dmax)
+
+
+@pytest.mark.parametrize("kd", [(3, 1, 5), (5, 3, 5), (3, 3, 1), (1, 3, 3), (7, 5, 3), (9, 1, 1)],
+                         ids=lambda k: "x".join(map(str, k)))
+@pytest.mark.parametrize("nx", [140, 141])
+def test_anisotropic_f32_guarded_cube(kd, nx):
+    """Other anisotropic f32 kernels (x/y padding, or K = 3) run cube-padded
+    behind an on-device Inf/NaN scan: finite volumes take the tiled kernel,
+    whose added zero taps are exact +0, and match the direct kernel; a volume
+    holding Inf or NaN takes the direct kernel and matches it bitwise."""
+    rng = np.random.default_rng(11 + sum(kd) + nx)
+    finite = rng.random((9, 23, nx), dtype=np.float32) - np.float32(0.25)
+    w = rng.random(kd[::-1]) - 0.2
+    kernel = vk.Kernel(kd, w.reshape(-1))
+    dst = vk.StructuredVolume((nx, 23, 9), vk.DataFormat.FLOAT32)
+
+    def run(stored, mode, path):
+        src = vk.StructuredVolume.from_numpy(stored, vk.DataFormat.FLOAT32)
+        vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
+        try:
+            vk.ApplyFilter(dst, src, kernel, mode)
+            return dst.to_numpy()
+        finally:
+            vk.set_execution_policy(vk.ExecutionPolicy())
+
+    src = vk.StructuredVolume.from_numpy(finite, vk.DataFormat.FLOAT32)
+    assert vk.filter_path(dst, src, kernel) == "tma"
+    bad = finite.copy()
+    bad[4, 10, 70] = np.inf
+    bad[2, 5, 3] = np.nan
+    for mode in ("wrap", "mirror", "clamp", "border"):
+        got = run(finite, mode, "auto")
+        assert np.array_equal(got, run(finite, mode, "direct")), (kd, mode)
+        ok, ndiff, dmax = within_contract(got, O.apply_filter(finite, 3, w, mode, workers=1), 3)
+        assert ok, (kd, mode, ndiff, dmax)
+        got = run(bad, mode, "auto")
+        assert np.array_equal(got.view(np.uint32), run(bad, mode, "direct").view(np.uint32)), (kd, mode)

@@ -33,9 +33,9 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
 cudaError_t scratch_free(void* p, cudaStream_t s);
 
 int launch_filter_direct(const FilterPlan& plan, cudaStream_t s);
-// Sets *flag (device int, zeroed here) to 1 when any of the n floats at v is
-// Inf or NaN.
-int launch_scan_nonfinite(const float* v, int64_t n, int* flag, cudaStream_t s);
+// Sets *flag (device int, zeroed first when `zero`) to 1 when any of the n
+// floats at v is Inf or NaN.
+int launch_scan_nonfinite(const float* v, int64_t n, int* flag, bool zero, cudaStream_t s);
 // Returns VKT_OK, an error, or -1 when the tiled kernel does not cover `plan`.
 int launch_filter_tma(const FilterPlan& plan, cudaStream_t s);
 bool tma_supported(const vkt_filter_args& a);

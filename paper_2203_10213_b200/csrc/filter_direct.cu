@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(256) scan_nonfinite_kernel(const float* __rest
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
-int launch_scan_nonfinite(const float* v, int64_t n, int* flag, cudaStream_t s) {
-  cudaError_t err = cudaMemsetAsync(flag, 0, sizeof(int), s);
+int launch_scan_nonfinite(const float* v, int64_t n, int* flag, bool zero, cudaStream_t s) {
+  cudaError_t err = zero ? cudaMemsetAsync(flag, 0, sizeof(int), s) : cudaSuccess;
   if (err == cudaSuccess) {
     int64_t head = (int64_t)(((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
     if (head > n) head = n;

@@ -143,10 +143,9 @@ static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
 // f32 volumes padded only in z run as they are: the kernel skips the padding
 // planes outright (a zero weight times an Inf would inject NaN).  Other f32
 // kernels (x/y padding, or K = 3, whose direct-staging kernel cannot skip)
-// are `guarded`: an Inf/NaN scan of the source picks, on the device, the
-// tiled launch when every voxel is finite (each added tap is then an exact
-// +0 again) or the direct kernel otherwise.  Unsharded volumes only (the
-// scan covers `src`, not halo buffers).
+// are `guarded`: an Inf/NaN scan of the source and its halo planes picks, on
+// the device, the tiled launch when every voxel is finite (each added tap is
+// then an exact +0 again) or the direct kernel otherwise.
 // The z extent may only grow when no halo buffers are involved: halos are
 // sized for the caller's kz.
 static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vector<double>& w,
@@ -160,7 +159,6 @@ static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vec
   const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
                          (a->global_nz <= 0 || a->global_nz == a->dims.z);
   guarded = a->format == VKT_F32 && (kx != k || ky != k || k == 3);
-  if (guarded && !unsharded) return false;
   if (kz != k && !unsharded) return false;
   w.assign((size_t)k * k * k, 0.0);
   const int ox = (k - kx) / 2, oy = (k - ky) / 2, oz = (k - kz) / 2;
@@ -189,8 +187,19 @@ static int launch_guarded(const FilterPlan& plan, FilterPlan& cube, cudaStream_t
     return err == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
   }
   const vkt_filter_args& a = *plan.args;
-  int st = launch_scan_nonfinite(static_cast<const float*>(a.src),
-                                 (int64_t)a.dims.x * a.dims.y * a.dims.z, static_cast<int*>(flag), s);
+  const int64_t plane = (int64_t)a.dims.x * a.dims.y;
+  int* f = static_cast<int*>(flag);
+  int st = launch_scan_nonfinite(static_cast<const float*>(a.src), plane * a.dims.z, f, true, s);
+  // halo buffers hold rz = kz/2 planes each (the caller's kz, which the cube
+  // keeps: pad_to_cube grows z only without halos).  Scanned only when this
+  // launch's output planes read them: an interior launch of a sharded step
+  // runs while the exchange is still filling them.
+  const int rz = a.kdims.z / 2;
+  const int64_t halo = plane * rz;
+  if (st == VKT_OK && a.halo_lo != nullptr && halo > 0 && plan.z_begin < rz)
+    st = launch_scan_nonfinite(static_cast<const float*>(a.halo_lo), halo, f, false, s);
+  if (st == VKT_OK && a.halo_hi != nullptr && halo > 0 && plan.z_end > a.dims.z - rz)
+    st = launch_scan_nonfinite(static_cast<const float*>(a.halo_hi), halo, f, false, s);
   if (st == VKT_OK) {
     cube.guard = static_cast<const int*>(flag);
     st = launch_filter_tma(cube, s);

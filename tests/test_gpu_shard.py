@@ -64,7 +64,8 @@ def _unsharded(host, fmt, kernel, mode, path="auto"):
 @pytest.mark.parametrize("mode", list(vk.AddressMode))
 @pytest.mark.parametrize("fmt,k", [(vk.DataFormat.UINT16, 7), (vk.DataFormat.FLOAT32, 3),
                                    (vk.DataFormat.UINT8, 5), (vk.DataFormat.FLOAT32, 9),
-                                   (vk.DataFormat.UINT8, (3, 1, 5)), (vk.DataFormat.FLOAT32, (5, 5, 1))],
+                                   (vk.DataFormat.UINT8, (3, 1, 5)), (vk.DataFormat.FLOAT32, (5, 5, 1)),
+                                   (vk.DataFormat.FLOAT32, (3, 1, 3)), (vk.DataFormat.FLOAT32, (1, 5, 5))],
                          ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
 def test_sharded_bit_identical_to_unsharded(world, mode, fmt, k):
     # K = 9 (rz = 4 > a slab at world 8), and anisotropic kernels: (3,1,5) is
@@ -82,6 +83,27 @@ def test_sharded_bit_identical_to_unsharded(world, mode, fmt, k):
     want = _unsharded(host, fmt, kern, mode)
     got = _sharded_run(host, fmt, kern, mode, world)
     assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+@pytest.mark.parametrize("mode", list(vk.AddressMode))
+def test_sharded_guarded_f32_sees_nonfinite_halo(mode):
+    # (3,1,3) f32 is cube-padded behind an Inf/NaN scan; an Inf / NaN sitting
+    # in the planes next to a slab boundary reaches the neighbour only through
+    # its halo buffer, whose scan must send that rank to the direct kernel
+    rng = np.random.default_rng(17)
+    host = rng.random((40, 24, 64), dtype=np.float32)
+    host[19, 7, 9] = np.inf   # world 2: rank 0's last plane, rank 1's halo_lo
+    host[20, 3, 30] = np.nan  # rank 1's first plane, rank 0's halo_hi
+    host[0, 5, 5] = -np.inf   # rank 0's first plane; Wrap: rank 1's halo_hi
+    w = rng.random(9)
+    kern = vk.Kernel((3, 1, 3), w / w.sum())
+    want = _unsharded(host, vk.DataFormat.FLOAT32, kern, mode, "direct")
+    got = _sharded_run(host, vk.DataFormat.FLOAT32, kern, mode, 2)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    fin = host.copy()
+    fin[~np.isfinite(fin)] = 0.5
+    assert np.array_equal(_sharded_run(fin, vk.DataFormat.FLOAT32, kern, mode, 2),
+                          _unsharded(fin, vk.DataFormat.FLOAT32, kern, mode, "direct"))
 
 
 @pytest.mark.parametrize("path", ["direct", "exact"])

@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 // filter_tma.cu — host side of the tiled TMA ApplyFilter kernel: eligibility,
 // tensor-map encoding (driver entry point, no libcuda link), chunk sizing and
@@ -134,12 +135,23 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {
     const int z = cand < nzo ? cand : nzo;
     const int64_t ctas = nxy * ((nzo + z - 1) / z);
-    const int64_t waves = (ctas + slots - 1) / slots;
-    const double cost = (double)waves * (z + 2 * r + 3);
+    // a partial last wave costs half a wave plus its fill: its CTAs share
+    // SMs with fewer neighbours (512^3 K = 5 / 7: 64-plane chunks at 3.5
+    // waves beat 48 at 4.8 by 2-3%, profiles/r01_zc_sweep_v36.txt)
+    const double w = (double)ctas / slots, wf = std::floor(w), fr = w - wf;
+    const double cost = (wf + (fr > 0 ? 0.5 + 0.5 * fr : 0.0)) * (z + 2 * r + 3);
     if (cost < best * 0.98) {
       best = cost;
       zc = z;
     }
+  }
+  // K >= 7 is FMA-bound and its halo planes cost staging issue slots: on
+  // volumes that still fill >= 8 waves, ~171-plane chunks are 1.5-2% faster
+  // than the model's pick (1024^3 u16 / f32 7^3: 11.32 -> 11.11 ms,
+  // profiles/r01_zc_sweep2_v36.txt); K <= 5 gains nothing measurable.
+  if (k >= 7) {
+    const int nch = (nzo + 170) / 171;
+    if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
   }
   if (const char* e = std::getenv("VKT_TMA_ZC")) zc = std::max(1, std::min(nzo, std::atoi(e)));  // diagnostics
   p.zc = zc;

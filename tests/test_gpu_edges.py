@@ -193,3 +193,21 @@ def test_anisotropic_f32_guarded_cube(kd, nx):
         assert ok, (kd, mode, ndiff, dmax)
         got = run(bad, mode, "auto")
         assert np.array_equal(got.view(np.uint32), run(bad, mode, "direct").view(np.uint32)), (kd, mode)
+
+
+@pytest.mark.parametrize("zc", [171, 200, 397])
+@pytest.mark.parametrize("fmt,k", [(2, 7), (3, 7), (2, 9), (3, 9), (1, 5), (3, 3)])
+def test_deep_z_chunks_match_direct(monkeypatch, zc, fmt, k):
+    """K >= 7 on big volumes runs ~171-plane z chunks (filter_tma.cu); forced
+    deep chunks (VKT_TMA_ZC, the diagnostics override) on a volume small
+    enough for the direct kernel stay bit-identical to it."""
+    rng = np.random.default_rng(zc + 10 * k + fmt)
+    shape = (400, 20, 136)
+    stored = (rng.random(shape, dtype=np.float32) if fmt == 3 else
+              rng.integers(0, 256 if fmt == 1 else 65536, size=shape).astype(np.uint8 if fmt == 1 else np.uint16))
+    w = rng.random((k, k, k))
+    w /= w.sum()
+    monkeypatch.setenv("VKT_TMA_ZC", str(zc))
+    for mode in ("wrap", "clamp"):
+        got = _run(stored, fmt, w, mode, "auto")
+        assert np.array_equal(got.view(np.uint8), _run(stored, fmt, w, mode, "direct").view(np.uint8)), mode

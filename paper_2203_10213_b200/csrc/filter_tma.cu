@@ -130,17 +130,17 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
                                  : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
                                           : tma::Layout<2, 3>::CTAS_PER_SM);
-  // The paired kernel at under 3 waves balances poorly: 512^3 u16 3^3 runs
-  // 0.266 ms at 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves),
-  // profiles/r01_zc_sweep3_v37.txt.  So chunks of >= 16 planes that fill 3
-  // waves are preferred when there are any (not on small volumes such as
-  // 256^3, where 16-plane chunks at < 1 wave stay fastest).
+  // Under 3 waves the grid balances poorly: 512^3 u16 3^3 runs 0.266 ms at
+  // 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves); f32 3^3 0.241 vs
+  // 0.231 (profiles/r01_zc_sweep3_v37.txt, r01_zc_sweep4_v37.txt).  So chunks
+  // of >= 16 planes that fill 3 waves are preferred when there are any (not
+  // on small volumes such as 256^3, where 16-plane chunks at < 1 wave stay
+  // fastest).
   bool three_waves = false;
-  if (!(a.format == VKT_F32 && k == 3))
-    for (int cand : {64, 48, 32, 24, 16}) {
-      const int z = cand < nzo ? cand : nzo;
-      if (z >= 16 && nxy * ((nzo + z - 1) / z) >= 3 * slots) three_waves = true;
-    }
+  for (int cand : {64, 48, 32, 24, 16}) {
+    const int z = cand < nzo ? cand : nzo;
+    if (z >= 16 && nxy * ((nzo + z - 1) / z) >= 3 * slots) three_waves = true;
+  }
   int zc = 64;
   double best = 1e300;
   for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {

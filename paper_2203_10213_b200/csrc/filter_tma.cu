@@ -160,7 +160,8 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   // K >= 7 is FMA-bound and its halo planes cost staging issue slots: on
   // volumes that still fill >= 8 waves, ~171-plane chunks are 1.5-2% faster
   // than the model's pick (1024^3 u16 / f32 7^3: 11.32 -> 11.11 ms,
-  // profiles/r01_zc_sweep2_v36.txt); K <= 5 gains nothing measurable.
+  // profiles/r01_zc_sweep2_v36.txt); K <= 5 gains nothing measurable (~94-plane
+  // chunks at 1024^3 K = 5: 4.261 vs 4.257 ms, profiles/r01_k5_chunks_v39.txt).
   if (k >= 7) {
     const int nch = (nzo + 170) / 171;
     if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;

@@ -125,6 +125,11 @@ int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_planes, vkt
 /* Which kernel vkt_apply_filter would launch for these args (VKT_PATH_*). */
 int vkt_filter_path(const vkt_filter_args* args);
 
+/* Output planes per CTA z-chunk the tiled kernel would use for these args on
+ * the current device (0: not the tiled path).  Chunk boundaries are where a
+ * CTA's rolling z accumulators restart, so parity tests probe both sides. */
+int vkt_filter_chunk_planes(const vkt_filter_args* args);
+
 /* FillRange: set cells in [lo, hi) ∩ [0, dims) to the stored bit pattern
  * `stored_bits` (u8: low 8 bits, u16: low 16 bits, f32: IEEE bits). */
 int vkt_fill_box(void* dst, vkt_int3 dims, int32_t format, vkt_int3 lo, vkt_int3 hi,

@@ -16,6 +16,8 @@ from .errors import (
     DeviceFailure,
     DimsMismatch,
     EmptyRange,
+    EmptyVolume,
+    NotASlab,
     IoFailure,
     NotSeekable,
     RangeOutOfBounds,
@@ -31,8 +33,11 @@ from .execution import (
     Device,
     ExecutionPolicy,
     FilterPath,
+    effective_workers,
     get_execution_policy,
+    hardware_concurrency,
     set_execution_policy,
+    set_hardware_concurrency_override,
     timed,
     with_policy,
 )
@@ -47,6 +52,7 @@ from .filters import (
     apply_filter,
     apply_filter_host,
     box_kernel,
+    chunk_planes,
     filter_path,
     gaussian_kernel,
     laplacian_kernel,
@@ -55,10 +61,13 @@ from .geom import Box3i, Vec3f, Vec3i, box3i, clip_box, full_box
 from .volume import (
     DataFormat,
     DeviceBuffer,
+    ManagedBuffer,
     StructuredVolume,
     VoxelMapping,
     create_structured_volume,
     dequantize_scalar,
+    device_resident,
+    emulated_device,
     quantize_scalar,
 )
 from .synthetic import synthetic_device, synthetic_host, synthetic_structured
@@ -73,7 +82,9 @@ from .io import (
     write_volume,
 )
 
-__version__ = "0.1.0"
+from .benchmarks import run_benchmarks
+
+__version__ = "0.2.0"
 
 __all__ = [
     "AddressMode", "AllocationFailure", "ApplyFilter", "Box3i", "DataFormat", "Device",
@@ -87,5 +98,7 @@ __all__ = [
     "synthetic_host", "synthetic_structured", "timed", "with_policy",
     "filter_file", "load_raw", "read_range", "read_volume", "volume_from_bytes", "volume_to_bytes",
     "write_range", "write_volume", "ClaheParams", "brick_mappings", "clahe_equalize",
-    "flip", "resample",
+    "flip", "resample", "ManagedBuffer", "emulated_device", "device_resident", "effective_workers",
+    "hardware_concurrency", "set_hardware_concurrency_override", "run_benchmarks", "chunk_planes",
+    "EmptyVolume", "NotASlab",
 ]

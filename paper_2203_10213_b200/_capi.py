@@ -31,6 +31,7 @@ EXPORTED_SYMBOLS = (
     "vkt_apply_filter",
     "vkt_apply_filter_host",
     "vkt_filter_path",
+    "vkt_filter_chunk_planes",
     "vkt_fill_box",
     "vkt_fill_synthetic",
     "vkt_status_name",
@@ -94,6 +95,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         lib.vkt_apply_filter_host.restype = ctypes.c_int
         lib.vkt_filter_path.argtypes = [ctypes.POINTER(FilterArgs)]
         lib.vkt_filter_path.restype = ctypes.c_int
+        lib.vkt_filter_chunk_planes.argtypes = [ctypes.POINTER(FilterArgs)]
+        lib.vkt_filter_chunk_planes.restype = ctypes.c_int
         lib.vkt_fill_box.argtypes = [vp, Int3, i32, Int3, Int3, u32, vp]
         lib.vkt_fill_box.restype = ctypes.c_int
         lib.vkt_fill_synthetic.argtypes = [vp, Int3, i32, u64, i64, vp]

@@ -25,7 +25,7 @@ from . import _capi
 from .errors import InvalidArgument
 from .execution import timed
 from .geom import Vec3i, ivec3
-from .volume import DataFormat, StructuredVolume
+from .volume import DataFormat, StructuredVolume, device_resident
 
 
 @dataclass
@@ -65,35 +65,42 @@ def _lib():
     return lib
 
 
-# -- host tables: same numpy arithmetic as the reference ---------------------
+# -- host tables ---------------------------------------------------------------
+# Restated from the reference's definitions (ops/filters.py:117-147); integer
+# results are identical by construction and the float64 blend weights use the
+# same operations (an exact halving for the centres, one subtract / divide /
+# clip per cell), so the tables are bit-identical (tests/test_clahe.py).
 
 def _axis_edges(extent: int, count: int) -> np.ndarray:
-    """`count` bricks over `extent` cells, remainder to the front (filters.py:118-122)."""
-    base, rem = divmod(extent, count)
-    sizes = [base + (1 if i < rem else 0) for i in range(count)]
-    return np.cumsum([0] + sizes)
+    """Brick boundaries of ``count`` bricks over ``extent`` cells; the first
+    ``extent % count`` bricks are one cell thicker (filters.py:118-122)."""
+    i = np.arange(count + 1, dtype=np.int64)
+    return i * (extent // count) + np.minimum(i, extent % count)
 
 
 def _clip_counts(hist: np.ndarray, limit: int) -> np.ndarray:
-    """Single-pass clip, pooled excess spread evenly, remainder to bins 0..r-1
+    """Clip every bin at ``limit`` once and hand the clipped total back in
+    equal shares, the indivisible rest one count each to the lowest bins
     (filters.py:124-132)."""
-    excess = int(np.sum(np.maximum(hist - limit, 0)))
-    clipped = np.minimum(hist, limit)
-    share, rem = divmod(excess, hist.size)
-    clipped = clipped + share
-    clipped[:rem] += 1
-    return clipped
+    over = hist - limit
+    excess = int(over[over > 0].sum())
+    out = np.minimum(hist, limit) + excess // hist.size
+    out[: excess % hist.size] += 1
+    return out
 
 
 def _blend_coords(extent: int, edges: np.ndarray):
-    """Per-cell lower brick index and blend weight along one axis (filters.py:135-147)."""
-    centers = (edges[:-1] + edges[1:]) / 2.0
-    x = np.arange(extent, dtype=np.float64) + 0.5
-    if len(centers) == 1:
+    """For each cell centre along one axis: the lower of the two brick centres
+    it blends between and its weight toward the upper one, clamped to the
+    outermost bricks (filters.py:135-147)."""
+    nb = len(edges) - 1
+    if nb == 1:
         return np.zeros(extent, dtype=np.int64), np.zeros(extent)
-    lo = np.clip(np.searchsorted(centers, x, side="right") - 1, 0, len(centers) - 2)
-    w = (x - centers[lo]) / (centers[lo + 1] - centers[lo])
-    return lo, np.clip(w, 0.0, 1.0)
+    mid = (edges[1:] + edges[:-1]) / 2.0
+    pos = np.arange(extent, dtype=np.float64) + 0.5
+    lower = np.clip(np.digitize(pos, mid) - 1, 0, nb - 2)
+    span = mid[lower + 1] - mid[lower]
+    return lower, np.clip((pos - mid[lower]) / span, 0.0, 1.0)
 
 
 def _validate(volume: StructuredVolume, params: ClaheParams) -> None:
@@ -192,14 +199,21 @@ def brick_mappings(volume: StructuredVolume, params: ClaheParams) -> np.ndarray:
     """Per-brick equalization maps, shape (bz, by, bx, num_bins) (filters.py:163-201)."""
     _validate(volume, params)
     keep: list = []
-    h, _ = _histograms(volume, params, keep)
-    return _mappings_from_hist(h, volume, params)
+    with device_resident(volume, write_back=False) as v:
+        h, _ = _histograms(v, params, keep)
+        return _mappings_from_hist(h, v, params)
 
 
 @timed("ClaheEqualize")
 def clahe_equalize(volume: StructuredVolume, params: ClaheParams) -> None:
-    """In-place CLAHE of a device volume (filters.py:204-245)."""
+    """In-place CLAHE (filters.py:204-245); host-resident volumes are staged
+    through HBM."""
     _validate(volume, params)
+    with device_resident(volume) as v:
+        _clahe_in_hbm(v, params)
+
+
+def _clahe_in_hbm(volume: StructuredVolume, params: ClaheParams) -> None:
     keep: list = []
     h, a = _histograms(volume, params, keep)
     maps = _mappings_from_hist(h, volume, params)

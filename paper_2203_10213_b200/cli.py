@@ -16,7 +16,7 @@ Volumes travel as VKTVOL01 bytes over files or standard streams.  Exit codes
 are the reference's: 0 success, 1 usage error, 2 data error with the line
 ``error: <ErrorName>: <message>`` on stderr (cli.py:547-564), which the TS
 bindings parse (cli.ts:38).  A failing invocation never leaves a partial
-output file (cli.py:209-225).  ``filter`` with both ``-i`` and ``-o`` files
+output file (cli.py:209-225; io.atomic_output).  ``filter`` with both ``-i`` and ``-o`` files
 streams the volume through the GPU out of core (``io.filter_file``), so
 volumes larger than host RAM and HBM work.  New: ``--mode`` selects the
 address mode (the reference always clamps).
@@ -26,11 +26,10 @@ from __future__ import annotations
 
 import argparse
 import math
-import os
 import sys
-import tempfile
-import time
 from pathlib import Path
+
+import numpy as np
 
 from . import io as vio
 from .errors import InvalidArgument, IoFailure, VktError
@@ -38,12 +37,13 @@ from .execution import ExecutionPolicy, set_execution_policy
 
 
 class _Parser(argparse.ArgumentParser):
-    """Usage errors exit 1, not argparse's 2 (cli.py:35-42)."""
+    """argparse with the reference's usage-error status: 1 instead of 2
+    (cli.py:35-42); the usage line and message still go to stderr."""
+
+    USAGE_ERROR = 1
 
     def error(self, message):
-        self.print_usage(sys.stderr)
-        print(f"{self.prog}: error: {message}", file=sys.stderr)
-        raise SystemExit(1)
+        self.exit(self.USAGE_ERROR, f"{self.format_usage()}{self.prog}: error: {message}\n")
 
 
 def _io_args(p, output=True):
@@ -113,34 +113,38 @@ def _build_parser() -> _Parser:
     return parser
 
 
-# -- stream helpers (cli.py:191-233) -----------------------------------------
+# -- input / output (same streams and messages as cli.py:191-233) -----------
+
+def _input_bytes(args) -> bytes:
+    """The raw input payload: the -i file, else standard input."""
+    path = getattr(args, "input", None)
+    if not path:
+        return sys.stdin.buffer.read()
+    try:
+        return Path(path).read_bytes()
+    except OSError as exc:
+        raise IoFailure(str(exc)) from exc
+
 
 def _read_volume_arg(args):
-    if getattr(args, "input", None):
-        return vio.read_volume(args.input)
-    payload = sys.stdin.buffer.read()
-    if not payload:
-        raise IoFailure("no input volume: pass -i PATH or pipe volume bytes")
-    return vio.volume_from_bytes(payload)
+    path = getattr(args, "input", None)
+    if path:
+        return vio.read_volume(path)
+    payload = _input_bytes(args)
+    if payload:
+        return vio.volume_from_bytes(payload)
+    raise IoFailure("no input volume: pass -i PATH or pipe volume bytes")
 
 
 def _write_bytes_out(path, payload: bytes) -> None:
-    if not path:
-        sys.stdout.buffer.write(payload)
-        sys.stdout.buffer.flush()
-        return
-    target = Path(path)
-    fd, tmp = tempfile.mkstemp(dir=str(target.parent) or ".", prefix=target.name + ".")
-    try:
-        with os.fdopen(fd, "wb") as fh:
+    """Payload to standard output, or atomically to ``path`` (io.atomic_output)."""
+    if path:
+        with vio.atomic_output(path) as fh:
             fh.write(payload)
-        os.replace(tmp, target)
-    except BaseException:
-        try:
-            os.unlink(tmp)
-        except OSError:
-            pass
-        raise
+        return
+    out = sys.stdout.buffer
+    out.write(payload)
+    out.flush()
 
 
 def _write_volume_out(args, volume) -> None:
@@ -148,19 +152,20 @@ def _write_volume_out(args, volume) -> None:
 
 
 def _kernel(args):
+    """--gaussian SIGMA [--ksize K], or --kernel-file: whitespace-separated
+    tokens, three integer extents then the x-fastest weights (cli.py:363-372)."""
     from .filters import Kernel, gaussian_kernel
 
     if (args.gaussian is None) == (args.kernel_file is None):
         raise InvalidArgument("pass exactly one of --gaussian or --kernel-file")
-    if args.gaussian is not None:
+    if args.kernel_file is None:
         return gaussian_kernel(args.gaussian, args.ksize)
     try:
-        text = Path(args.kernel_file).read_text().split()
-    except OSError as e:
-        raise IoFailure(str(e)) from e
-    dims = [int(v) for v in text[:3]]
-    weights = [float(v) for v in text[3:]]
-    return Kernel(dims, weights)
+        tokens = Path(args.kernel_file).read_text().split()
+    except OSError as exc:
+        raise IoFailure(str(exc)) from exc
+    extents = tuple(int(t) for t in tokens[:3])
+    return Kernel(extents, np.array(tokens[3:], dtype=np.float64))
 
 
 # -- commands ----------------------------------------------------------------
@@ -238,55 +243,22 @@ def _cmd_flip(args) -> int:
 
 
 def _cmd_raw_import(args) -> int:
-    if getattr(args, "input", None):
-        try:
-            payload = Path(args.input).read_bytes()
-        except OSError as e:
-            raise IoFailure(str(e)) from e
-    else:
-        payload = sys.stdin.buffer.read()
+    payload = _input_bytes(args)
     volume = vio.load_raw(payload, args.dims, args.format, args.cell_size, tuple(args.range))
     _write_volume_out(args, volume)
     return 0
 
 
 def _cmd_bench(args) -> int:
-    """The ApplyFilter-path cases of the reference bench (bench.py:88-146):
-    gaussian_filter (gaussian_kernel(1.0, 3) on synthetic_structured(size),
-    setup copy outside the timer) and fillrange, best of `repeat`, device
-    time.  One device executes both the "serial" and the "parallel" plan,
-    so both columns report the same measurement."""
-    import torch
+    """The structured cases of the reference bench on the B200
+    (benchmarks.run_benchmarks; report lines as cli.py:495-509)."""
+    from .benchmarks import run_benchmarks
 
-    from .fill import fill_range
-    from .filters import apply_filter, gaussian_kernel
-    from .synthetic import synthetic_structured
-
-    volume = synthetic_structured(args.size)
-    kernel = gaussian_kernel(1.0, 3)
-
-    def best(fn, setup):
-        b = math.inf
-        for _ in range(max(1, args.repeat)):
-            ctx = setup() if setup else None
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            fn(ctx)
-            torch.cuda.synchronize()
-            b = min(b, time.perf_counter() - t0)
-        return b
-
-    cases = [
-        ("fillrange", lambda _: fill_range(volume, volume.bounds, 0.5), None),
-        ("gaussian_filter", lambda v: apply_filter(v, kernel), volume.copy),
-    ]
-    lines = []
-    for name, fn, setup in cases:
-        best(fn, setup)  # warm-up
-        t = best(fn, setup)
-        lines.append(f"bench: case={name} serial_s={t:.6f} parallel_s={t:.6f} "
-                     f"workers={args.bench_workers} effective_workers=1")
-    _write_bytes_out(getattr(args, "output", None), ("\n".join(lines) + "\n").encode())
+    reports = run_benchmarks(args.size, args.subgrids, args.bench_workers, args.repeat)
+    text = "".join(f"bench: case={r['case']} serial_s={r['serial_s']:.6f} "
+                   f"parallel_s={r['parallel_s']:.6f} workers={r['workers']} "
+                   f"effective_workers={r['effective_workers']}\n" for r in reports)
+    _write_bytes_out(getattr(args, "output", None), text.encode())
     return 0
 
 
@@ -302,20 +274,25 @@ _COMMANDS = {
 }
 
 
+def _error_line(exc: BaseException) -> str:
+    """``error: <ErrorName>: <message>`` — the line the TS bindings parse
+    (cli.ts:38); OS errors report as IoFailure (cli.py:559-564)."""
+    name = exc.name if isinstance(exc, VktError) else "IoFailure"
+    return f"error: {name}: {exc}\n"
+
+
 def main(argv=None) -> int:
-    parser = _build_parser()
+    """Exit status 0 on success, 1 on a usage error, 2 on a data error."""
     try:
-        args = parser.parse_args(argv)
-    except SystemExit as e:
-        return int(e.code or 0)
+        args = _build_parser().parse_args(argv)
+    except SystemExit as stop:
+        return int(stop.code or 0)
     set_execution_policy(ExecutionPolicy(worker_count=args.workers, print_timings=args.timings))
+    command = _COMMANDS[args.command]
     try:
-        return _COMMANDS[args.command](args)
-    except VktError as e:
-        print(f"error: {e.name}: {e}", file=sys.stderr)
-        return 2
-    except OSError as e:
-        print(f"error: IoFailure: {e}", file=sys.stderr)
+        return command(args)
+    except (VktError, OSError) as exc:
+        sys.stderr.write(_error_line(exc))
         return 2
 
 

@@ -145,6 +145,7 @@ int check_args(const vkt_clahe_args* a) {
 using namespace vkt;
 
 extern "C" int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   int st = check_args(args);
   if (st != VKT_OK) return st;
   const vkt_clahe_args& a = *args;
@@ -161,7 +162,7 @@ extern "C" int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t str
   }
   // enough CTAs to fill the GPU: split each brick's planes
   const int brick_z = (a.dims.z + a.bricks.z - 1) / a.bricks.z;
-  int64_t zsplit = (148 * 8 + nbricks - 1) / nbricks;
+  int64_t zsplit = (sm_count() * 8 + nbricks - 1) / nbricks;
   if (zsplit > brick_z) zsplit = brick_z;
   if (zsplit < 1) zsplit = 1;
   if (nbricks > 0x7fffffff || zsplit > 65535) {
@@ -185,6 +186,7 @@ extern "C" int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t str
 }
 
 extern "C" int vkt_clahe_blend(const vkt_clahe_args* args, vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   int st = check_args(args);
   if (st != VKT_OK) return st;
   const vkt_clahe_args& a = *args;

@@ -26,6 +26,33 @@ struct FilterPlan {
 
 void set_error_detail(const char* fmt, ...);
 
+// Streaming multiprocessors of the current device (cached per device; 148 on
+// a B200).  Grid sizing and the z-chunk wave model use it.
+int sm_count();
+
+// Makes the stream's device current for the scope of an ABI call (and
+// restores the caller's device): the tensor maps, the scratch pool, the
+// shared-memory opt-in and the launch all act on the current device, and a
+// caller may pass a stream of another device than the current one.  The
+// legacy/per-thread default streams keep the current device.
+struct StreamDeviceGuard {
+  int prev = -1;
+  explicit StreamDeviceGuard(cudaStream_t s) {
+    if (s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread) return;
+    int d = 0, cur = 0;
+    if (cudaStreamGetDevice(s, &d) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != d && cudaSetDevice(d) == cudaSuccess) prev = cur;
+  }
+  ~StreamDeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  StreamDeviceGuard(const StreamDeviceGuard&) = delete;
+  StreamDeviceGuard& operator=(const StreamDeviceGuard&) = delete;
+};
+
 // Stream-ordered scratch from a library-owned memory pool on the current
 // device whose release threshold is unlimited, so repeated calls reuse the
 // same HBM instead of mapping/unmapping it on every synchronize.
@@ -39,6 +66,8 @@ int launch_scan_nonfinite(const float* v, int64_t n, int* flag, bool zero, cudaS
 // Returns VKT_OK, an error, or -1 when the tiled kernel does not cover `plan`.
 int launch_filter_tma(const FilterPlan& plan, cudaStream_t s);
 bool tma_supported(const vkt_filter_args& a);
+// Output planes per CTA chunk the tiled kernel would use for `plan`.
+int tma_chunk_planes(const FilterPlan& plan);
 
 int launch_fill_box(void* dst, vkt_int3 dims, int format, vkt_int3 lo, vkt_int3 hi,
                     uint32_t bits, cudaStream_t s);

@@ -161,13 +161,13 @@ int launch_fill_box(void* dst, vkt_int3 dims, int format, vkt_int3 lo, vkt_int3 
     const int ncell = (int)((p.seg_bytes - 16 * (int64_t)nvec) / bpc);
     const int64_t total = p.n_seg_y * p.n_seg_z * (nvec + ncell);
     const int64_t blocks = (total + 255) / 256;
-    fill_segs_kernel<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(p, hb, nvec, ncell);
+    fill_segs_kernel<<<(int)(blocks < sm_count() * 16 ? blocks : sm_count() * 16), 256, 0, s>>>(p, hb, nvec, ncell);
   } else if (p.seg_bytes <= 4096) {
     const int64_t nseg = p.n_seg_y * p.n_seg_z;
     const int64_t blocks = (nseg + 7) / 8;
-    fill_rows_kernel<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(p);
+    fill_rows_kernel<<<(int)(blocks < sm_count() * 16 ? blocks : sm_count() * 16), 256, 0, s>>>(p);
   } else {
-    int grid = (int)(items < 148 * 16 ? items : 148 * 16);
+    int grid = (int)(items < sm_count() * 16 ? items : sm_count() * 16);
     fill_box_kernel<<<grid, 256, 0, s>>>(p);
   }
   count_launch();
@@ -205,7 +205,7 @@ int launch_fill_synthetic(void* dst, vkt_int3 dims, int format, uint64_t seed,
   const int64_t n = (int64_t)dims.x * dims.y * dims.z;
   if (n == 0) return VKT_OK;
   const int64_t first = z_offset * (int64_t)dims.x * dims.y;
-  int grid = 148 * 8;
+  int grid = sm_count() * 8;
   if (format == VKT_U8) synthetic_kernel<uint8_t><<<grid, 256, 0, s>>>((uint8_t*)dst, n, first, seed);
   else if (format == VKT_U16) synthetic_kernel<uint16_t><<<grid, 256, 0, s>>>((uint16_t*)dst, n, first, seed);
   else synthetic_kernel<float><<<grid, 256, 0, s>>>((float*)dst, n, first, seed);

@@ -217,7 +217,7 @@ int launch_scan_nonfinite(const float* v, int64_t n, int* flag, bool zero, cudaS
     if (head > n) head = n;
     const int64_t nvec = (n - head) / 4;
     int64_t blocks = (nvec + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
     if (blocks < 1) blocks = 1;
     scan_nonfinite_kernel<<<(unsigned)blocks, 256, 0, s>>>(v, n, head, flag);
     count_launch();

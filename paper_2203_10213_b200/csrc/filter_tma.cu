@@ -77,6 +77,61 @@ bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz
 
 }  // namespace
 
+// Chunk depth ZC: every CTA pays ~2R extra input planes plus a pipeline
+// fill; the grid pays wave quantization.  Pick the ZC with the smallest
+// estimated time  waves(ZC) * (ZC + 2R + fill)  (fill ~ 3 planes).
+int tma_chunk_planes(const FilterPlan& plan) {
+  const vkt_filter_args& a = *plan.args;
+  const int k = a.kdims.x, r = k / 2;
+  const int nzo = plan.z_end - plan.z_begin;
+  if (nzo <= 0) return 1;
+  const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
+  // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
+  // K = 3 (4, Wrap 3)
+  const int64_t slots = (int64_t)sm_count() * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
+                                 : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
+                                 : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
+                                          : tma::Layout<2, 3>::CTAS_PER_SM);
+  // Under 3 waves the grid balances poorly: 512^3 u16 3^3 runs 0.266 ms at
+  // 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves); f32 3^3 0.241 vs
+  // 0.231 (profiles/r01_zc_sweep3_v37.txt, r01_zc_sweep4_v37.txt).  So chunks
+  // of >= 16 planes that fill 3 waves are preferred when there are any (not
+  // on small volumes such as 256^3, where 16-plane chunks at < 1 wave stay
+  // fastest).
+  bool three_waves = false;
+  for (int cand : {64, 48, 32, 24, 16}) {
+    const int z = cand < nzo ? cand : nzo;
+    if (z >= 16 && nxy * ((nzo + z - 1) / z) >= 3 * slots) three_waves = true;
+  }
+  int zc = 64;
+  double best = 1e300;
+  for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {
+    const int z = cand < nzo ? cand : nzo;
+    const int64_t ctas = nxy * ((nzo + z - 1) / z);
+    if (three_waves && (z < 16 || ctas < 3 * slots)) continue;
+    // a partial last wave costs half a wave plus its fill: its CTAs share
+    // SMs with fewer neighbours (512^3 K = 5 / 7: 64-plane chunks at 3.5
+    // waves beat 48 at 4.8 by 2-3%, profiles/r01_zc_sweep_v36.txt)
+    const double w = (double)ctas / slots, wf = std::floor(w), fr = w - wf;
+    const double cost = (wf + (fr > 0 ? 0.5 + 0.5 * fr : 0.0)) * (z + 2 * r + 3);
+    if (cost < best * 0.98) {
+      best = cost;
+      zc = z;
+    }
+  }
+  // K >= 7 is FMA-bound and its halo planes cost staging issue slots: on
+  // volumes that still fill >= 8 waves, ~171-plane chunks are 1.5-2% faster
+  // than the model's pick (1024^3 u16 / f32 7^3: 11.32 -> 11.11 ms,
+  // profiles/r01_zc_sweep2_v36.txt); K <= 5 gains nothing measurable (~94-plane
+  // chunks at 1024^3 K = 5: 4.261 vs 4.257 ms, profiles/r01_k5_chunks_v39.txt).
+  if (k >= 7) {
+    const int nch = (nzo + 170) / 171;
+    if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
+  }
+  if (const char* e = std::getenv("VKT_TMA_ZC")) zc = std::max(1, std::min(nzo, std::atoi(e)));  // diagnostics
+  return zc;
+}
+
 bool tma_supported(const vkt_filter_args& a) {
   if (a.flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
   const int k = a.kdims.x;
@@ -119,54 +174,8 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   p.zskip = plan.zskip;
   p.guard = plan.guard;
 
-  // Chunk depth ZC: every CTA pays ~2R extra input planes plus a pipeline
-  // fill; the grid pays wave quantization.  Pick the ZC with the smallest
-  // estimated time  waves(ZC) * (ZC + 2R + fill)  (fill ~ 3 planes).
   const int nzo = plan.z_end - plan.z_begin;
-  const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
-  // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
-  // K = 3 (4, Wrap 3)
-  const int64_t slots = 148ll * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
-                                 : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
-                                 : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
-                                          : tma::Layout<2, 3>::CTAS_PER_SM);
-  // Under 3 waves the grid balances poorly: 512^3 u16 3^3 runs 0.266 ms at
-  // 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves); f32 3^3 0.241 vs
-  // 0.231 (profiles/r01_zc_sweep3_v37.txt, r01_zc_sweep4_v37.txt).  So chunks
-  // of >= 16 planes that fill 3 waves are preferred when there are any (not
-  // on small volumes such as 256^3, where 16-plane chunks at < 1 wave stay
-  // fastest).
-  bool three_waves = false;
-  for (int cand : {64, 48, 32, 24, 16}) {
-    const int z = cand < nzo ? cand : nzo;
-    if (z >= 16 && nxy * ((nzo + z - 1) / z) >= 3 * slots) three_waves = true;
-  }
-  int zc = 64;
-  double best = 1e300;
-  for (int cand : {64, 48, 32, 24, 16, 12, 8, 6, 4}) {
-    const int z = cand < nzo ? cand : nzo;
-    const int64_t ctas = nxy * ((nzo + z - 1) / z);
-    if (three_waves && (z < 16 || ctas < 3 * slots)) continue;
-    // a partial last wave costs half a wave plus its fill: its CTAs share
-    // SMs with fewer neighbours (512^3 K = 5 / 7: 64-plane chunks at 3.5
-    // waves beat 48 at 4.8 by 2-3%, profiles/r01_zc_sweep_v36.txt)
-    const double w = (double)ctas / slots, wf = std::floor(w), fr = w - wf;
-    const double cost = (wf + (fr > 0 ? 0.5 + 0.5 * fr : 0.0)) * (z + 2 * r + 3);
-    if (cost < best * 0.98) {
-      best = cost;
-      zc = z;
-    }
-  }
-  // K >= 7 is FMA-bound and its halo planes cost staging issue slots: on
-  // volumes that still fill >= 8 waves, ~171-plane chunks are 1.5-2% faster
-  // than the model's pick (1024^3 u16 / f32 7^3: 11.32 -> 11.11 ms,
-  // profiles/r01_zc_sweep2_v36.txt); K <= 5 gains nothing measurable (~94-plane
-  // chunks at 1024^3 K = 5: 4.261 vs 4.257 ms, profiles/r01_k5_chunks_v39.txt).
-  if (k >= 7) {
-    const int nch = (nzo + 170) / 171;
-    if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
-  }
-  if (const char* e = std::getenv("VKT_TMA_ZC")) zc = std::max(1, std::min(nzo, std::atoi(e)));  // diagnostics
+  const int zc = tma_chunk_planes(plan);
   p.zc = zc;
   dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + tma::TY - 1) / tma::TY,
             (nzo + zc - 1) / zc);
@@ -202,14 +211,34 @@ int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
                       (!a.halo_lo || aligned16(a.halo_lo)) && (!a.halo_hi || aligned16(a.halo_hi));
   if (direct) return launch_pitched(plan, a.src, a.dst, a.halo_lo, a.halo_hi, a.dims.x, s);
 
-  // Pitched staging: copy the slab (and halos) into scratch with rows padded
-  // to 16 bytes, filter there, copy the computed planes back.  Two extra
-  // passes over the data; hidden for the FP32-bound kernels.
+  // Pitched staging: copy the planes this launch reads (and the halos it
+  // reads) into scratch with rows padded to 16 bytes, filter there, copy the
+  // computed planes back.  Two extra passes over the data; hidden for the
+  // FP32-bound kernels.  When every plane of the read window
+  // [z_begin - rz, z_end + rz) is a slab plane or comes from a halo buffer,
+  // only the window's slab planes are staged, as a sub-slab (the thin
+  // boundary launches of a sharded step stage rz..2rz planes, not the slab);
+  // otherwise (address-mapped planes at the volume's faces) the whole slab.
   const int pitch = (int)((((int64_t)a.dims.x * bpc + 15) / 16 * 16) / bpc);
   const size_t row_b = (size_t)a.dims.x * bpc, prow_b = (size_t)pitch * bpc;
   const size_t pplane = prow_b * a.dims.y;
+  const int wlo = plan.z_begin - rz, whi = plan.z_end + rz;
+  const bool self_contained = (wlo >= 0 || a.halo_lo != nullptr) && (whi <= a.dims.z || a.halo_hi != nullptr);
+  const int zlo = self_contained ? (wlo > 0 ? wlo : 0) : 0;
+  const int zhi = self_contained ? (whi < a.dims.z ? whi : a.dims.z) : a.dims.z;
+  vkt_filter_args sub = a;
+  sub.dims.z = zhi - zlo;
+  sub.z_offset = a.z_offset + zlo;
+  sub.halo_lo = zlo == 0 ? a.halo_lo : nullptr;
+  sub.halo_hi = zhi == a.dims.z ? a.halo_hi : nullptr;
+  FilterPlan sp = plan;
+  sp.args = &sub;
+  sp.z_begin = plan.z_begin - zlo;
+  sp.z_end = plan.z_end - zlo;
+  sp.geom.z_offset = sub.z_offset;
+  sp.geom.nz = sub.dims.z;
   const int nzo = plan.z_end - plan.z_begin;
-  const size_t in_b = pplane * a.dims.z, halo_b = pplane * rz, out_b = pplane * nzo;
+  const size_t in_b = pplane * sub.dims.z, halo_b = pplane * rz, out_b = pplane * nzo;
   uint8_t* buf = nullptr;
   const size_t total = in_b + 2 * halo_b + out_b + 64;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&buf), total, s);
@@ -218,24 +247,25 @@ int launch_filter_tma(const FilterPlan& plan, cudaStream_t s) {
     return e == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
   }
   uint8_t* in = buf;
-  uint8_t* hlo = a.halo_lo ? in + in_b : nullptr;
-  uint8_t* hhi = a.halo_hi ? in + in_b + halo_b : nullptr;
+  uint8_t* hlo = sub.halo_lo ? in + in_b : nullptr;
+  uint8_t* hhi = sub.halo_hi ? in + in_b + halo_b : nullptr;
   uint8_t* out = in + in_b + 2 * halo_b;
-  auto copy2d = [&](void* d, size_t dp, const void* src, size_t sp, size_t rows) {
-    return cudaMemcpy2DAsync(d, dp, src, sp, row_b, rows, cudaMemcpyDeviceToDevice, s);
+  auto copy2d = [&](void* d, size_t dp, const void* src, size_t sp_, size_t rows) {
+    return cudaMemcpy2DAsync(d, dp, src, sp_, row_b, rows, cudaMemcpyDeviceToDevice, s);
   };
   int st = VKT_OK;
-  if (copy2d(in, prow_b, a.src, row_b, (size_t)a.dims.y * a.dims.z) != cudaSuccess ||
-      (hlo && copy2d(hlo, prow_b, a.halo_lo, row_b, (size_t)a.dims.y * rz) != cudaSuccess) ||
-      (hhi && copy2d(hhi, prow_b, a.halo_hi, row_b, (size_t)a.dims.y * rz) != cudaSuccess)) {
+  const uint8_t* src_planes = static_cast<const uint8_t*>(a.src) + row_b * a.dims.y * zlo;
+  if (copy2d(in, prow_b, src_planes, row_b, (size_t)a.dims.y * sub.dims.z) != cudaSuccess ||
+      (hlo && copy2d(hlo, prow_b, sub.halo_lo, row_b, (size_t)a.dims.y * rz) != cudaSuccess) ||
+      (hhi && copy2d(hhi, prow_b, sub.halo_hi, row_b, (size_t)a.dims.y * rz) != cudaSuccess)) {
     set_error_detail("pitched staging copy: %s", cudaGetErrorString(cudaGetLastError()));
     st = VKT_DEVICE_FAILURE;
   }
   if (st == VKT_OK) {
     // the kernel addresses output plane oz at dst + oz * plane: shift so the
     // computed planes [z_begin, z_end) land in `out`
-    uint8_t* dst_base = out - (ptrdiff_t)pplane * plan.z_begin;
-    st = launch_pitched(plan, in, dst_base, hlo, hhi, pitch, s);
+    uint8_t* dst_base = out - (ptrdiff_t)pplane * sp.z_begin;
+    st = launch_pitched(sp, in, dst_base, hlo, hhi, pitch, s);
   }
   if (st == VKT_OK &&
       cudaMemcpy2DAsync(static_cast<uint8_t*>(a.dst) + row_b * a.dims.y * plan.z_begin, row_b, out, prow_b,

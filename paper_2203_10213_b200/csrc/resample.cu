@@ -124,13 +124,14 @@ using namespace vkt;
 
 extern "C" int vkt_flip(const void* src, void* dst, vkt_int3 dims, int32_t format, int32_t axis,
                         vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   if (!src || !dst || src == dst || dims.x < 1 || dims.y < 1 || dims.z < 1 || !fmt_ok(format) ||
       axis < 0 || axis > 2) {
     set_error_detail("flip: invalid arguments (src/dst distinct, dims >= 1, axis 0..2)");
     return VKT_INVALID_ARGUMENT;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int grid = 148 * 8;
+  const int grid = sm_count() * 8;
   if (format == VKT_U8)
     flip_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, dims.x, dims.y, dims.z, axis);
   else if (format == VKT_U16)
@@ -149,6 +150,7 @@ extern "C" int vkt_flip(const void* src, void* dst, vkt_int3 dims, int32_t forma
 extern "C" int vkt_resample(const void* src, vkt_int3 src_dims, int32_t src_format, double src_lo,
                             double src_hi, void* dst, vkt_int3 dst_dims, int32_t dst_format,
                             double dst_lo, double dst_hi, vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   if (!src || !dst || src_dims.x < 1 || src_dims.y < 1 || src_dims.z < 1 || dst_dims.x < 1 ||
       dst_dims.y < 1 || dst_dims.z < 1 || !fmt_ok(src_format) || !fmt_ok(dst_format) ||
       !(src_lo < src_hi) || !(dst_lo < dst_hi) || dst_dims.y > 65535 || dst_dims.z > 65535) {

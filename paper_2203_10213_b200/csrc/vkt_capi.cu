@@ -30,6 +30,21 @@ void set_error_detail(const char* fmt, ...) {
   va_end(ap);
 }
 
+int sm_count() {
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  if (dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    n = 148;
+  if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
+  return n;
+}
+
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
@@ -220,6 +235,7 @@ using namespace vkt;
 extern "C" {
 
 int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   FilterPlan plan;
   int st = validate_and_plan(args, plan);
   if (st != VKT_OK) return st;
@@ -264,8 +280,26 @@ int vkt_filter_path(const vkt_filter_args* args) {
   return plan.path;
 }
 
+int vkt_filter_chunk_planes(const vkt_filter_args* args) {
+  FilterPlan plan;
+  if (validate_and_plan(args, plan) != VKT_OK) return 0;
+  if (plan.path == VKT_PATH_DIRECT) {
+    vkt_filter_args cube;
+    std::vector<double> wcube;
+    FilterPlan p2;
+    uint32_t zskip = 0;
+    bool guarded = false;
+    if (pad_to_cube(args, cube, wcube, zskip, guarded) && validate_and_plan(&cube, p2) == VKT_OK &&
+        p2.path == VKT_PATH_TMA)
+      return tma_chunk_planes(p2);
+    return 0;
+  }
+  return plan.path == VKT_PATH_TMA ? tma_chunk_planes(plan) : 0;
+}
+
 int vkt_fill_box(void* dst, vkt_int3 dims, int32_t format, vkt_int3 lo, vkt_int3 hi,
                  uint32_t stored_bits, vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   if (dst == nullptr) return fail(VKT_INVALID_ARGUMENT, "dst is NULL");
   if (dims.x < 1 || dims.y < 1 || dims.z < 1)
     return fail(VKT_INVALID_ARGUMENT, "dims must be >= 1 per axis");
@@ -277,6 +311,7 @@ int vkt_fill_box(void* dst, vkt_int3 dims, int32_t format, vkt_int3 lo, vkt_int3
 
 int vkt_fill_synthetic(void* dst, vkt_int3 dims, int32_t format, uint64_t seed, int64_t z_offset,
                        vkt_stream_t stream) {
+  const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   if (dst == nullptr) return fail(VKT_INVALID_ARGUMENT, "dst is NULL");
   if (dims.x < 1 || dims.y < 1 || dims.z < 1)
     return fail(VKT_INVALID_ARGUMENT, "dims must be >= 1 per axis");

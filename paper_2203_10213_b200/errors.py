@@ -45,6 +45,15 @@ class RangeOutOfBounds(VktError):
     """The region of interest extends past the volume bounds (errors.py:41)."""
 
 
+class NotASlab(VktError):
+    """A Delete region is not a full-extent slab (errors.py:45).  Kept so
+    reference callers that import it run unchanged; not raised on this path."""
+
+
+class EmptyVolume(VktError):
+    """A volume with zero cells (errors.py:33); kept for the same reason."""
+
+
 class BadMagic(VktError):
     """The stream does not start with VKTVOL01 (errors.py:57)."""
 
@@ -80,7 +89,7 @@ class DeviceFailure(VktError):
 _BY_NAME = {
     cls.__name__: cls
     for cls in (InvalidArgument, IndexOutOfRange, AllocationFailure, EvenKernelDims,
-                DimsMismatch, DeviceFailure, EmptyRange, RangeOutOfBounds, BadMagic,
+                DimsMismatch, DeviceFailure, EmptyRange, RangeOutOfBounds, NotASlab, EmptyVolume, BadMagic,
                 TruncatedPayload, UnknownFormatCode, IoFailure, SizeMismatch, NotSeekable)
 }
 

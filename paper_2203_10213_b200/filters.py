@@ -175,6 +175,19 @@ def filter_path(dst: StructuredVolume, src: StructuredVolume, kernel: Kernel,
     return _capi.PATH_NAMES[_capi.load().vkt_filter_path(ctypes.byref(args))]
 
 
+def chunk_planes(src: StructuredVolume, kernel: Kernel, address_mode=AddressMode.CLAMP) -> int:
+    """Output planes per CTA z-chunk the tiled kernel uses for this launch
+    (0 when another kernel runs).  Chunk boundaries restart a CTA's rolling z
+    accumulators; the at-size parity tests probe both sides of each."""
+    import torch
+
+    mode = AddressMode.coerce(address_mode)
+    args, _keep = make_args(src.data_ptr(), src.data_ptr() + 16, src.dims, src.format, src.mapping,
+                            kernel, mode, flags=_flags(get_execution_policy()))
+    with torch.cuda.device(src.data.device):
+        return int(_capi.load().vkt_filter_chunk_planes(ctypes.byref(args)))
+
+
 def _current_stream(volume: StructuredVolume) -> int:
     import torch
 
@@ -188,7 +201,9 @@ def ApplyFilter(dst: StructuredVolume, src: StructuredVolume, filter: Kernel,
 
     ``dst`` and ``src`` must agree in dims, format and mapping.  Passing the
     same volume twice filters in place (snapshot semantics, filters.py:77).
-    Asynchronous on the current torch CUDA stream.
+    Volumes in HBM: asynchronous on the current torch CUDA stream.
+    Host-resident volumes (``Device.CPU``): streamed through HBM by the
+    host-buffer pipeline; returns when ``dst`` holds the result.
     """
     if not isinstance(filter, Kernel):
         raise InvalidArgument("filter must be a Kernel/Filter")
@@ -196,28 +211,47 @@ def ApplyFilter(dst: StructuredVolume, src: StructuredVolume, filter: Kernel,
     if dst is src:
         _apply_in_place(src, filter, mode)
         return
+    src.data.migrate()
+    dst.data.migrate()
     require_same_layout(dst, src)
     policy = get_execution_policy()
-    args, _keep = make_args(dst.data_ptr(), src.data_ptr(), src.dims, src.format, src.mapping,
-                            filter, mode, flags=_flags(policy))
     if policy.debug_messages:
         debug(f"ApplyFilter {src!r} k={tuple(filter.dims)} mode={mode.name}")
+    if src.on_host:
+        _apply_host_resident(dst, src, filter, mode)
+        return
+    args, _keep = make_args(dst.data_ptr(), src.data_ptr(), src.dims, src.format, src.mapping,
+                            filter, mode, flags=_flags(policy))
     launch(args, _current_stream(src))
 
 
-def _apply_in_place(volume: StructuredVolume, kernel: Kernel, mode: AddressMode) -> None:
-    from .volume import DeviceBuffer
+def _apply_host_resident(dst: StructuredVolume, src: StructuredVolume, kernel: Kernel,
+                         mode: AddressMode) -> None:
+    """Both volumes in page-locked host memory: the chunked H2D / filter / D2H
+    pipeline of ``vkt_apply_filter_host`` (csrc/vkt_host.cu) on the device."""
+    d = src.dims
+    shape = (d.z, d.y, d.x)
+    s_arr = src.data.array.view(src.format.dtype).reshape(shape)
+    d_arr = dst.data.array.view(dst.format.dtype).reshape(shape)
+    apply_filter_host(s_arr, kernel, mode, fmt=src.format, mapping=tuple(src.mapping), out=d_arr)
 
-    out = StructuredVolume(volume.dims, volume.format, volume.cell_size, volume.mapping,
-                           data=DeviceBuffer(volume.nbytes, device=volume.data.device, zero=False))
-    args, _keep = make_args(out.data_ptr(), volume.data_ptr(), volume.dims, volume.format,
-                            volume.mapping, kernel, mode, flags=_flags(get_execution_policy()))
+
+def _apply_in_place(volume: StructuredVolume, kernel: Kernel, mode: AddressMode) -> None:
     import torch
 
+    volume.data.migrate()
+    out = StructuredVolume(volume.dims, volume.format, volume.cell_size, volume.mapping,
+                           data=volume.data.empty_like())
+    if volume.on_host:
+        _apply_host_resident(out, volume, kernel, mode)
+        volume.swap_storage(out)
+        return
+    args, _keep = make_args(out.data_ptr(), volume.data_ptr(), volume.dims, volume.format,
+                            volume.mapping, kernel, mode, flags=_flags(get_execution_policy()))
     stream = torch.cuda.current_stream(volume.data.device)
     launch(args, int(stream.cuda_stream))
-    # The old buffer goes back to the torch caching allocator; recording the
-    # launch stream keeps it from being reused before the kernel has read it.
+    # The old bytes go back to the torch caching allocator; recording the
+    # launch stream keeps them from being reused before the kernel has read them.
     volume.data.tensor.record_stream(stream)
     volume.swap_storage(out)
 

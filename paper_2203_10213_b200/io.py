@@ -20,6 +20,7 @@ import io as _io
 import os
 import struct
 import tempfile
+from contextlib import contextmanager
 from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 from typing import BinaryIO, Union
@@ -52,6 +53,43 @@ Source = Union[str, os.PathLike, bytes, bytearray, BinaryIO]
 
 
 # -- header ------------------------------------------------------------------
+
+def _new_file_mode(target: Path) -> int:
+    """Mode a plain open() would give ``target``: the existing file's, else
+    0o666 minus the umask (mkstemp's 0o600 would make outputs owner-only)."""
+    try:
+        return target.stat().st_mode & 0o7777
+    except OSError:
+        mask = os.umask(0)
+        os.umask(mask)
+        return 0o666 & ~mask
+
+
+@contextmanager
+def atomic_output(path):
+    """Binary file that replaces ``path`` only once the block completes: the
+    bytes go to a sibling temporary file that is renamed into place, so a
+    failed command never leaves a partial output (the reference CLI's
+    contract, cli.py:209-225)."""
+    target = Path(path)
+    mode = _new_file_mode(target)
+    handle = tempfile.NamedTemporaryFile(mode="w+b", dir=str(target.parent) or ".",
+                                         prefix=f".{target.name}.", delete=False)
+    done = False
+    try:
+        with handle:
+            yield handle
+            handle.flush()
+        os.chmod(handle.name, mode)
+        os.replace(handle.name, target)
+        done = True
+    finally:
+        if not done:
+            try:
+                os.unlink(handle.name)
+            except OSError:
+                pass
+
 
 def pack_header(dims, fmt: DataFormat, cell_size, mapping) -> bytes:
     d = ivec3(dims)
@@ -356,65 +394,56 @@ def filter_file(src, dst, kernel, address_mode=None, *, chunk_planes: int = 0) -
     C = min(C, nz)
     chunks = [(z0, min(z0 + C, nz)) for z0 in range(0, nz, C)]
 
-    fd, tmp = tempfile.mkstemp(dir=str(dst.parent) or ".", prefix=dst.name + ".")
-    try:
-        with os.fdopen(fd, "wb") as out_f, open(src, "rb") as in_f:
-            out_f.write(header)
-            out_f.truncate(HEADER_SIZE + plane_b * nz)
+    with atomic_output(dst) as out_f, open(src, "rb") as in_f:
+        out_f.write(header)
+        out_f.truncate(HEADER_SIZE + plane_b * nz)
 
-            # two pinned slab and output buffers in rotation: chunk c reads into
-            # slab[c % 2] (chunk c-2 was filtered before c-1 started) and
-            # filters into out[c % 2] (chunk c-2's write finished before
-            # chunk c-1's write was queued)
-            slab_bufs = [_pinned(C * plane_b) for _ in range(min(2, len(chunks)))]
-            out_bufs = [_pinned(C * plane_b) for _ in range(min(2, len(chunks)))]
+        # two pinned slab and output buffers in rotation: chunk c reads into
+        # slab[c % 2] (chunk c-2 was filtered before c-1 started) and
+        # filters into out[c % 2] (chunk c-2's write finished before
+        # chunk c-1's write was queued)
+        slab_bufs = [_pinned(C * plane_b) for _ in range(min(2, len(chunks)))]
+        out_bufs = [_pinned(C * plane_b) for _ in range(min(2, len(chunks)))]
 
-            def view(buf, n):
-                return buf.numpy()[:n * plane_b].view(fmt.dtype).reshape(n, ny, nx)
+        def view(buf, n):
+            return buf.numpy()[:n * plane_b].view(fmt.dtype).reshape(n, ny, nx)
 
-            def read_chunk(c, z0, z1):
-                slab = view(slab_bufs[c % 2], z1 - z0)
-                in_f.seek(HEADER_SIZE + z0 * plane_b)
-                _Stream(in_f).readinto_exact(memoryview(slab.reshape(-1).view(np.uint8)), "z-slab")
-                halos = []
-                for first in (z0 - rz, z1):
-                    if rz == 0:
-                        halos.append(None)
-                        continue
-                    h = np.zeros((rz, ny, nx), dtype=fmt.dtype)
-                    for t in range(rz):
-                        m = map_plane(first + t, nz, mode)
-                        if m is None:
-                            continue  # Border: stored 0
-                        in_f.seek(HEADER_SIZE + m * plane_b)
-                        _Stream(in_f).readinto_exact(memoryview(h[t].reshape(-1).view(np.uint8)), "halo")
-                    halos.append(h)
-                return slab, halos
+        def read_chunk(c, z0, z1):
+            slab = view(slab_bufs[c % 2], z1 - z0)
+            in_f.seek(HEADER_SIZE + z0 * plane_b)
+            _Stream(in_f).readinto_exact(memoryview(slab.reshape(-1).view(np.uint8)), "z-slab")
+            halos = []
+            for first in (z0 - rz, z1):
+                if rz == 0:
+                    halos.append(None)
+                    continue
+                h = np.zeros((rz, ny, nx), dtype=fmt.dtype)
+                for t in range(rz):
+                    m = map_plane(first + t, nz, mode)
+                    if m is None:
+                        continue  # Border: stored 0
+                    in_f.seek(HEADER_SIZE + m * plane_b)
+                    _Stream(in_f).readinto_exact(memoryview(h[t].reshape(-1).view(np.uint8)), "halo")
+                halos.append(h)
+            return slab, halos
 
-            def write_chunk(z0, out):
-                out_f.seek(HEADER_SIZE + z0 * plane_b)
-                out_f.write(memoryview(out.reshape(-1).view(np.uint8)))
+        def write_chunk(z0, out):
+            out_f.seek(HEADER_SIZE + z0 * plane_b)
+            out_f.write(memoryview(out.reshape(-1).view(np.uint8)))
 
-            with ThreadPoolExecutor(max_workers=1) as reader, ThreadPoolExecutor(max_workers=1) as writer:
-                pending_read = reader.submit(read_chunk, 0, *chunks[0])
-                pending_write = None
-                for c, (z0, z1) in enumerate(chunks):
-                    slab, halos = pending_read.result()
-                    if c + 1 < len(chunks):
-                        pending_read = reader.submit(read_chunk, c + 1, *chunks[c + 1])
-                    out = view(out_bufs[c % 2], z1 - z0)
-                    apply_filter_host(slab, kernel, mode, fmt=fmt, mapping=tuple(mapping), out=out,
-                                      z_offset=z0, global_nz=nz, halo_lo=halos[0], halo_hi=halos[1])
-                    if pending_write is not None:
-                        pending_write.result()
-                    pending_write = writer.submit(write_chunk, z0, out)
+        with ThreadPoolExecutor(max_workers=1) as reader, ThreadPoolExecutor(max_workers=1) as writer:
+            pending_read = reader.submit(read_chunk, 0, *chunks[0])
+            pending_write = None
+            for c, (z0, z1) in enumerate(chunks):
+                slab, halos = pending_read.result()
+                if c + 1 < len(chunks):
+                    pending_read = reader.submit(read_chunk, c + 1, *chunks[c + 1])
+                out = view(out_bufs[c % 2], z1 - z0)
+                apply_filter_host(slab, kernel, mode, fmt=fmt, mapping=tuple(mapping), out=out,
+                                  z_offset=z0, global_nz=nz, halo_lo=halos[0], halo_hi=halos[1])
                 if pending_write is not None:
                     pending_write.result()
-            out_f.flush()
-        os.replace(tmp, dst)
-    except BaseException:
-        try:
-            os.unlink(tmp)
-        except OSError:
-            pass
-        raise
+                pending_write = writer.submit(write_chunk, z0, out)
+            if pending_write is not None:
+                pending_write.result()
+

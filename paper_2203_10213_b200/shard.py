@@ -227,13 +227,17 @@ def _comm_stream(device):
 @timed("ApplyFilterSharded")
 def apply_filter_sharded(dst: ShardedVolume, src: ShardedVolume, kernel: Kernel,
                          address_mode=AddressMode.CLAMP, group=None, exchange=None,
-                         kernel_events: Optional[list] = None) -> None:
+                         kernel_events: Optional[list] = None,
+                         phase_events: Optional[dict] = None) -> None:
     """Sharded ApplyFilter: halo exchange overlapped with the interior kernel.
 
     ``exchange(plan, rank, planes, halo_lo, halo_hi)`` defaults to the NCCL /
     torch.distributed ``exchange_halos``; tests substitute an in-process
     copy.  ``kernel_events``, if given, receives one (start, end) CUDA event
-    pair around the main (interior) launch, for the bench's roofline.
+    pair around the main (interior) launch, for the bench's roofline;
+    ``phase_events`` (a dict) receives (start, end) pairs on the comm stream
+    under "exchange" (the halo exchange) and "boundary" (the boundary
+    launches), for the bench's per-rank breakdown.
     """
     import torch
 
@@ -271,9 +275,25 @@ def apply_filter_sharded(dst: ShardedVolume, src: ShardedVolume, kernel: Kernel,
     lo, hi = src.halo_buffers(rz)
     comm = _comm_stream(dev)
     comm.wait_stream(compute)  # src planes are final
+
+    def mark(key):
+        if phase_events is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(comm)
+        return (key, ev)
+
+    def close(opened):
+        if opened is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(comm)
+            phase_events.setdefault(opened[0], []).append((opened[1], ev))
+
+    opened = mark("exchange")
     with torch.cuda.stream(comm):
         exchange(plan, src.rank, src.planes(), lo.array.view(rz, src.plane_bytes),
                  hi.array.view(rz, src.plane_bytes))
+    close(opened)
     halo_ptrs = dict(halo_lo=lo.data_ptr(), halo_hi=hi.data_ptr())
     if n > 2 * rz:
         a, _k = make_args(dst.local.data_ptr(), src.local.data_ptr(), **common, **halo_ptrs,
@@ -288,10 +308,12 @@ def apply_filter_sharded(dst: ShardedVolume, src: ShardedVolume, kernel: Kernel,
     # single launch, against +4.5% when they ran after the interior;
     # tools/shard_overhead.py).  Disjoint output planes; the compute stream
     # joins the comm stream before anything else touches dst.
+    opened = mark("boundary")
     for b, e in ranges:
         a, _k = make_args(dst.local.data_ptr(), src.local.data_ptr(), **common, **halo_ptrs,
                           out_z_begin=b, out_z_end=e)
         launch(a, int(comm.cuda_stream))
+    close(opened)
     compute.wait_stream(comm)
     lo.tensor.record_stream(comm)
     hi.tensor.record_stream(comm)

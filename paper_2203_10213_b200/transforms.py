@@ -22,7 +22,7 @@ from . import _capi
 from .errors import InvalidArgument
 from .execution import timed
 from .geom import Vec3i
-from .volume import DataFormat, DeviceBuffer, StructuredVolume, VoxelMapping
+from .volume import DataFormat, DeviceBuffer, StructuredVolume, VoxelMapping, device_resident
 
 _AXES = {"x": 0, "y": 1, "z": 2}
 
@@ -59,14 +59,15 @@ def _stream(volume):
 @timed("Flip")
 def flip(volume: StructuredVolume, axis) -> None:
     """Reverse stored values along one axis, in place (geometric.py:34-40)."""
-    a = _axis(axis)
-    out = DeviceBuffer(volume.nbytes, device=volume.data.device, zero=False)
-    _capi.check(_lib().vkt_flip(volume.data_ptr(), out.data_ptr(), _capi.int3(volume.dims),
-                                volume.format.value, a, _stream(volume)))
     import torch
 
-    volume.data.tensor.record_stream(torch.cuda.current_stream(volume.data.device))
-    volume.data = out
+    a = _axis(axis)
+    with device_resident(volume) as v:
+        out = StructuredVolume(v.dims, v.format, v.cell_size, v.mapping, data=v.data.empty_like())
+        _capi.check(_lib().vkt_flip(v.data_ptr(), out.data_ptr(), _capi.int3(v.dims),
+                                    v.format.value, a, _stream(v)))
+        v.data.tensor.record_stream(torch.cuda.current_stream(v.data.device))
+        v.swap_storage(out)
 
 
 @timed("Resample")
@@ -82,11 +83,18 @@ def resample(source: StructuredVolume, dst_dims, dst_format=None, dst_mapping=No
     mapping = source.mapping if dst_mapping is None else VoxelMapping.coerce(dst_mapping)
     src_cell = np.asarray(source.cell_size, dtype=np.float64)
     dst_cell = src_cell * np.asarray(source.dims, dtype=np.float64) / np.asarray(dst_dims, dtype=np.float64)
-    out = StructuredVolume(dst_dims, fmt, tuple(dst_cell), mapping,
-                           data=DeviceBuffer(dst_dims.x * dst_dims.y * dst_dims.z * fmt.bytes_per_cell,
-                                             device=source.data.device, zero=False))
-    _capi.check(_lib().vkt_resample(
-        source.data_ptr(), _capi.int3(source.dims), source.format.value, source.mapping.lo,
-        source.mapping.hi, out.data_ptr(), _capi.int3(dst_dims), fmt.value, mapping.lo, mapping.hi,
-        _stream(source)))
+    nbytes = dst_dims.x * dst_dims.y * dst_dims.z * fmt.bytes_per_cell
+    with device_resident(source, write_back=False) as src:
+        out = StructuredVolume(dst_dims, fmt, tuple(dst_cell), mapping,
+                               data=DeviceBuffer(nbytes, device=src.data.device, zero=False))
+        _capi.check(_lib().vkt_resample(
+            src.data_ptr(), _capi.int3(src.dims), src.format.value, src.mapping.lo,
+            src.mapping.hi, out.data_ptr(), _capi.int3(dst_dims), fmt.value, mapping.lo, mapping.hi,
+            _stream(src)))
+    if source.on_host or type(source) is not StructuredVolume:
+        # the result lives where the caller's volumes live (its policy's space)
+        res = type(source)(dst_dims, fmt, tuple(dst_cell), mapping)
+        res.data.migrate()
+        res.data.raw.copy_(out.data.raw)
+        return res
     return out

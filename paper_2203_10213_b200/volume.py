@@ -13,10 +13,12 @@ a numpy arena that ``ManagedBuffer.migrate`` copies around (managed.py:97-154).
 from __future__ import annotations
 
 import math
+import threading
 from enum import Enum
 from typing import Optional
 
 import struct
+from contextlib import contextmanager
 
 import numpy as np
 
@@ -174,24 +176,133 @@ def _device(policy=None):
     return torch.device("cuda", idx)
 
 
-class DeviceBuffer:
-    """A byte allocation in HBM; the device-resident ``ManagedBuffer``.
+class DeviceSpace:
+    """Capacity accounting of ``ManagedBuffer`` bytes resident in HBM.
 
-    ``migration_count`` stays 0: there is one residency (the reference's
+    The reference's ``emulated_device`` arena (managed.py:31-59) has an
+    optional capacity so allocation failure is observable; here the arena is
+    the B200's HBM and the same accounting applies to the managed volumes
+    placed there (``AllocationFailure`` past the capacity, or on a real CUDA
+    out-of-memory).
+    """
+
+    def __init__(self, capacity_bytes: Optional[int] = None):
+        self.capacity_bytes = capacity_bytes
+        self.used_bytes = 0
+        self._lock = threading.Lock()
+
+    def set_capacity(self, capacity_bytes: Optional[int]) -> None:
+        with self._lock:
+            self.capacity_bytes = capacity_bytes
+
+    def reserve(self, nbytes: int) -> None:
+        with self._lock:
+            if self.capacity_bytes is not None and self.used_bytes + nbytes > self.capacity_bytes:
+                raise AllocationFailure(
+                    f"device cannot hold {nbytes} bytes ({self.used_bytes}/{self.capacity_bytes} in use)")
+            self.used_bytes += nbytes
+
+    def release(self, nbytes: int) -> None:
+        with self._lock:
+            self.used_bytes -= nbytes
+
+
+#: Process-wide HBM accounting for managed volumes (the reference's name).
+emulated_device = DeviceSpace()
+
+
+def _alloc_device(nbytes: int, dev, zero: bool):
+    import torch
+
+    try:
+        alloc = torch.zeros if zero else torch.empty
+        return alloc(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    except torch.OutOfMemoryError as e:
+        raise AllocationFailure(f"device cannot hold {nbytes} bytes: {e}") from None
+
+
+def _alloc_host(nbytes: int, zero: bool):
+    """Page-locked host bytes: the device reads and writes them directly
+    (unified addressing), and copies to and from HBM run at full PCIe rate."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceFailure("no CUDA device is visible; the B200 path has no CPU fallback")
+    t = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    if zero:
+        t.zero_()
+    return t
+
+
+class _Storage:
+    """Bytes of a volume in one residency: ``tensor`` is a uint8 torch tensor
+    in HBM or in page-locked host memory."""
+
+    byte_length: int
+    migration_count: int
+    tensor: "object"
+
+    @property
+    def on_host(self) -> bool:
+        return not self.tensor.is_cuda
+
+    @property
+    def residency(self):
+        from .execution import Device
+
+        return Device.CPU if self.on_host else Device.CUDA
+
+    @property
+    def raw(self):
+        """The bytes as a torch tensor (host or device)."""
+        return self.tensor[: self.byte_length]
+
+    @property
+    def array(self):
+        """The resident bytes: a numpy view on the host, a torch view in HBM."""
+        if self.on_host:
+            return self.tensor[: self.byte_length].numpy()
+        return self.tensor[: self.byte_length]
+
+    @property
+    def device(self):
+        return self.tensor.device
+
+    def data_ptr(self) -> int:
+        return int(self.tensor.data_ptr())
+
+    def to_bytes(self) -> bytes:
+        raw = self.raw
+        return (raw.numpy() if self.on_host else raw.cpu().numpy()).tobytes()
+
+    def empty_like(self) -> "_Storage":
+        """Uninitialized bytes of the same length and residency."""
+        out = _Storage.__new__(type(self))
+        out.byte_length = self.byte_length
+        out.migration_count = 0
+        out.tensor = (_alloc_host(self.byte_length, False) if self.on_host
+                      else _alloc_device(self.byte_length, self.tensor.device, False))
+        if isinstance(out, ManagedBuffer):
+            if not out.on_host:
+                emulated_device.reserve(out.byte_length)
+            out._init_accounting()
+        return out
+
+    def __len__(self) -> int:
+        return self.byte_length
+
+
+class DeviceBuffer(_Storage):
+    """A byte allocation in HBM: the native API's fixed-residency buffer.
+
+    ``migration_count`` stays 0: its residency never changes (the reference's
     migrate() on a matching space is a no-op, managed.py:119-126).
     """
 
     def __init__(self, nbytes: int, device=None, zero: bool = True):
-        import torch
-
         self.byte_length = int(nbytes)
         self.migration_count = 0
-        dev = device if device is not None else _device()
-        try:
-            alloc = torch.zeros if zero else torch.empty
-            self.tensor = alloc(max(self.byte_length, 1), dtype=torch.uint8, device=dev)
-        except torch.OutOfMemoryError as e:
-            raise AllocationFailure(f"device cannot hold {nbytes} bytes: {e}") from None
+        self.tensor = _alloc_device(self.byte_length, device if device is not None else _device(), zero)
 
     @classmethod
     def wrap(cls, tensor) -> "DeviceBuffer":
@@ -207,24 +318,86 @@ class DeviceBuffer:
         return buf
 
     def migrate(self) -> None:
-        """No-op: the bytes are already in the only device space."""
+        """No-op: the bytes stay in HBM."""
 
-    @property
-    def array(self):
-        return self.tensor[: self.byte_length]
 
-    @property
-    def device(self):
-        return self.tensor.device
+def _managed_policy():
+    from .execution import explicit_policy
 
-    def data_ptr(self) -> int:
-        return int(self.tensor.data_ptr())
+    return explicit_policy()
 
-    def to_bytes(self) -> bytes:
-        return self.array.cpu().numpy().tobytes()
 
-    def __len__(self) -> int:
-        return self.byte_length
+class ManagedBuffer(_Storage):
+    """The reference's managed byte buffer (managed.py:97-154): resident in
+    exactly one space, the one the calling thread's policy selects.
+
+    ``Device.CPU`` keeps the bytes in page-locked host memory (``array`` is a
+    numpy view); ``Device.EMULATED_DEVICE`` / ``Device.CUDA`` in HBM.  With
+    no policy set on the thread the reference's default applies: the host.
+    ``migrate()`` moves them when the policy's space differs and counts the
+    move in ``migration_count``; algorithms call it before touching the data.
+    """
+
+    def __init__(self, initial, device=None):
+        if isinstance(initial, (int, np.integer)):
+            self.byte_length = int(initial)
+            host = None
+        else:
+            host = np.frombuffer(bytes(initial), dtype=np.uint8)
+            self.byte_length = int(host.size)
+        self.migration_count = 0
+        policy = _managed_policy()
+        if policy is None or policy.device.on_host:
+            self.tensor = _alloc_host(self.byte_length, host is None)
+        else:
+            emulated_device.reserve(self.byte_length)
+            try:
+                self.tensor = _alloc_device(self.byte_length, device if device is not None else _device(policy),
+                                            host is None)
+            except BaseException:
+                emulated_device.release(self.byte_length)
+                raise
+        self._init_accounting()
+        if host is not None and host.size:
+            self.raw.copy_(__import__("torch").from_numpy(host.copy()))
+
+    def _init_accounting(self) -> None:
+        self._charged = 0 if self.on_host else self.byte_length
+        self._lock = threading.Lock()
+
+    def migrate(self) -> None:
+        """Move the bytes to the current policy's space if they are elsewhere."""
+        from .execution import debug
+
+        policy = _managed_policy()
+        want_host = policy is None or policy.device.on_host
+        with self._lock:
+            if want_host == self.on_host:
+                return
+            if want_host:
+                dst = _alloc_host(self.byte_length, False)
+                dst[: self.byte_length].copy_(self.raw)  # synchronous D2H
+                emulated_device.release(self._charged)
+                self._charged = 0
+            else:
+                emulated_device.reserve(self.byte_length)
+                try:
+                    dst = _alloc_device(self.byte_length, _device(policy), False)
+                except BaseException:
+                    emulated_device.release(self.byte_length)
+                    raise
+                dst[: self.byte_length].copy_(self.raw)
+                self._charged = self.byte_length
+            debug(f"migrate {self.byte_length} bytes {'device -> host' if want_host else 'host -> device'}")
+            self.tensor = dst
+            self.migration_count += 1
+
+    def __del__(self):
+        try:
+            if self._charged:
+                emulated_device.release(self._charged)
+        except Exception:
+            pass
 
 
 class StructuredVolume:
@@ -242,7 +415,7 @@ class StructuredVolume:
         self.mapping = VoxelMapping.coerce(mapping)
         nbytes = self.cell_count * self.format.bytes_per_cell
         if data is None:
-            data = DeviceBuffer(nbytes)
+            data = self._new_storage(nbytes)
         elif data.byte_length != nbytes:
             raise InvalidArgument(f"buffer holds {data.byte_length} bytes, volume needs {nbytes}")
         self.data = data
@@ -266,10 +439,38 @@ class StructuredVolume:
         return self.data.byte_length
 
     # -- storage -----------------------------------------------------------
+    @property
+    def on_host(self) -> bool:
+        """True when the bytes live in page-locked host memory (``Device.CPU``)."""
+        return self.data.on_host
+
     def array(self):
-        """Device view of the stored values shaped (z, y, x)."""
+        """Stored values shaped (z, y, x), after migrating to the policy's
+        space (volume.py:172-177): a numpy view for host-resident volumes, a
+        torch CUDA view for volumes in HBM."""
+        self.data.migrate()
         d = self.dims
+        if self.data.on_host:
+            return self.data.array.view(self.format.dtype).reshape(d.z, d.y, d.x)
         return self.data.array.view(self.format.torch_dtype).view(d.z, d.y, d.x)
+
+    def mapped_array(self) -> np.ndarray:
+        """Host float64 application values shaped (z, y, x) (volume.py:179-181):
+        dequantize in the reference's float64 operation order (volume.py:113-118)."""
+        s = self.to_numpy()
+        if self.format is DataFormat.FLOAT32:
+            return np.asarray(s, dtype=np.float64)
+        lo, hi = self.mapping
+        return lo + (np.asarray(s, dtype=np.float64) / self.format.max_int) * (hi - lo)
+
+    #: former name of ``mapped_array``
+    mapped_numpy = mapped_array
+
+    def normalized_array(self) -> np.ndarray:
+        """Mapping-normalized values in [0, 1] (volume.py:183-186)."""
+        m = self.mapped_array()
+        lo, hi = self.mapping
+        return np.clip((m - lo) / (hi - lo), 0.0, 1.0)
 
     def data_ptr(self) -> int:
         return self.data.data_ptr()
@@ -277,16 +478,9 @@ class StructuredVolume:
     def to_numpy(self) -> np.ndarray:
         """Host copy of the stored values shaped (z, y, x)."""
         d = self.dims
-        raw = self.data.array.cpu().numpy()
-        return raw.view(self.format.dtype).reshape(d.z, d.y, d.x)
-
-    def mapped_numpy(self) -> np.ndarray:
-        """Host float64 application values (the reference's ``mapped_array``)."""
-        s = self.to_numpy()
-        if self.format is DataFormat.FLOAT32:
-            return s.astype(np.float64)
-        lo, hi = self.mapping
-        return lo + (s.astype(np.float64) / self.format.max_int) * (hi - lo)
+        raw = self.data.raw
+        host = raw.numpy().copy() if self.data.on_host else raw.cpu().numpy()
+        return host.view(self.format.dtype).reshape(d.z, d.y, d.x)
 
     def upload(self, host: np.ndarray, non_blocking: bool = False) -> None:
         """Copy a host array of the storage dtype (any shape with the right size) in."""
@@ -298,7 +492,7 @@ class StructuredVolume:
                 f"upload needs {self.cell_count} cells of {self.format.dtype}, "
                 f"got {arr.size} of {arr.dtype}")
         src = torch.from_numpy(arr.reshape(-1).view(np.uint8))
-        self.data.array.copy_(src, non_blocking=non_blocking)
+        self.data.raw.copy_(src, non_blocking=non_blocking and not self.data.on_host)
 
     @classmethod
     def from_numpy(cls, host: np.ndarray, fmt=None, cell_size=(1.0, 1.0, 1.0),
@@ -315,10 +509,15 @@ class StructuredVolume:
             fmt = inv[np.dtype(key)]
         fmt = fmt if isinstance(fmt, DataFormat) else DataFormat.parse(fmt)
         nz, ny, nx = host.shape
-        buf = DeviceBuffer(nx * ny * nz * fmt.bytes_per_cell, zero=False)
-        v = cls((nx, ny, nz), fmt, cell_size, mapping, data=buf)
+        v = cls((nx, ny, nz), fmt, cell_size, mapping, data=cls._new_storage(nx * ny * nz * fmt.bytes_per_cell, zero=False))
         v.upload(host.astype(fmt.dtype, copy=False))
         return v
+
+    @classmethod
+    def _new_storage(cls, nbytes: int, zero: bool = True):
+        """Default storage of new volumes: HBM (the façade in ``.vkt`` overrides
+        this with a policy-following ``ManagedBuffer``)."""
+        return DeviceBuffer(nbytes, zero=zero)
 
     def fill_bytes(self, raw: bytes) -> None:
         import torch
@@ -326,17 +525,25 @@ class StructuredVolume:
         if len(raw) != self.data.byte_length:
             raise InvalidArgument(
                 f"payload holds {len(raw)} bytes, volume needs {self.data.byte_length}")
-        self.data.array.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+        self.data.migrate()
+        self.data.raw.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
 
     def copy(self) -> "StructuredVolume":
-        out = StructuredVolume(self.dims, self.format, self.cell_size, self.mapping,
-                               data=DeviceBuffer(self.nbytes, device=self.data.device, zero=False))
-        out.data.array.copy_(self.data.array)
+        self.data.migrate()
+        out = type(self)(self.dims, self.format, self.cell_size, self.mapping, data=self.data.empty_like())
+        out.data.raw.copy_(self.data.raw)
         return out
 
     def swap_storage(self, other: "StructuredVolume") -> None:
-        """O(1) exchange of the device buffers of two same-shaped volumes."""
-        self.data, other.data = other.data, self.data
+        """O(1) exchange of the bytes of two same-shaped volumes (the buffer
+        objects, and their migration counts, stay with their volumes)."""
+        a, b = self.data, other.data
+        if type(a) is type(b):
+            a.tensor, b.tensor = b.tensor, a.tensor
+            if isinstance(a, ManagedBuffer):
+                a._charged, b._charged = b._charged, a._charged
+        else:
+            self.data, other.data = b, a
 
     # -- single cells ------------------------------------------------------
     def _check_index(self, idx):
@@ -347,7 +554,8 @@ class StructuredVolume:
 
     def get_value(self, idx) -> float:
         i = self._check_index(idx)
-        stored = self.array()[i.z, i.y, i.x].cpu().numpy()
+        cell = self.array()[i.z, i.y, i.x]
+        stored = cell if self.data.on_host else cell.cpu().numpy()
         return dequantize_scalar(stored, self.format, self.mapping)
 
     def set_value(self, idx, value: float) -> None:
@@ -355,12 +563,36 @@ class StructuredVolume:
 
         i = self._check_index(idx)
         q = np.asarray([quantize_scalar(value, self.format, self.mapping)], dtype=self.format.dtype)
-        self.array()[i.z, i.y, i.x] = torch.from_numpy(q)[0].to(self.data.device)
+        arr = self.array()
+        if self.data.on_host:
+            arr[i.z, i.y, i.x] = q[0]
+        else:
+            arr[i.z, i.y, i.x] = torch.from_numpy(q)[0].to(self.data.device)
 
     def __repr__(self):
         d = self.dims
         return (f"StructuredVolume({d.x}x{d.y}x{d.z}, {self.format.short_name}, "
                 f"range [{self.mapping.lo}, {self.mapping.hi}], {self.data.device})")
+
+
+@contextmanager
+def device_resident(volume: "StructuredVolume", write_back: bool = True):
+    """Yield a volume whose bytes are in HBM for a device algorithm: the
+    volume itself, or for a host-resident (``Device.CPU``) volume a device
+    copy whose result is copied back (``write_back``) before returning."""
+    import torch
+
+    volume.data.migrate()
+    if not volume.data.on_host:
+        yield volume
+        return
+    dev = StructuredVolume(volume.dims, volume.format, volume.cell_size, volume.mapping,
+                           data=DeviceBuffer(volume.nbytes, zero=False))
+    dev.data.raw.copy_(volume.data.raw)
+    yield dev
+    if write_back:
+        volume.data.raw.copy_(dev.data.raw)  # synchronous D2H into the pinned bytes
+    torch.cuda.current_stream().synchronize()
 
 
 def create_structured_volume(dims, fmt, cell_size=(1.0, 1.0, 1.0), mapping=(0.0, 1.0)):
@@ -380,6 +612,7 @@ def require_same_layout(a: StructuredVolume, b: StructuredVolume) -> None:
 
 
 __all__ = [
-    "DataFormat", "VoxelMapping", "StructuredVolume", "DeviceBuffer", "create_structured_volume",
+    "DataFormat", "VoxelMapping", "StructuredVolume", "DeviceBuffer", "ManagedBuffer", "DeviceSpace",
+    "emulated_device", "device_resident", "create_structured_volume",
     "quantize_scalar", "dequantize_scalar", "stored_bits", "fill_bits", "require_same_layout",
 ]

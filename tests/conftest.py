@@ -70,19 +70,38 @@ def load_fill_cases():
     return out
 
 
-def within_contract(got: np.ndarray, ref: np.ndarray, fmt: int):
+def within_contract(got: np.ndarray, ref: np.ndarray, fmt: int, weights):
     """BASELINE.md §5 parity contract for the fast (f32-accumulate) path.
 
-    ints: |got - ref| <= 1 LSB.  f32: |got - ref| <= 1e-5*|ref| + 1e-5
-    (rtol 1e-5 from the north star plus the reference's own 1e-5 absolute
-    criterion, pkg/tests/test_acceptance.py:65-70).
+    ints: |got - ref| <= 1 LSB.
+    f32: |got - ref| <= 1e-5 * |ref| — the north star's rtol 1e-5.  Only a
+    kernel with negative weights (the zero-sum Laplacian, random signed
+    kernels) adds the reference's own 1e-5 absolute term
+    (pkg/tests/test_acceptance.py:65-70): its outputs cancel toward 0, where a
+    relative bound on an FP32 sum is meaningless (Laplacian
+    max rel 1.6e-3 on near-zero voxels at max abs 9.5e-7).
     Returns (ok, n_differing, max_abs_diff).
     """
     if fmt == 3:
         g = got.astype(np.float64)
         r = ref.astype(np.float64)
         d = np.abs(g - r)
-        ok = bool(np.all(d <= 1e-5 * np.abs(r) + 1e-5))
-        return ok, int((d > 0).sum()), float(d.max(initial=0.0))
+        atol = 1e-5 if bool((np.asarray(weights) < 0).any()) else 0.0
+        both_nan = np.isnan(g) & np.isnan(r)
+        ok = bool(np.all((d <= 1e-5 * np.abs(r) + atol) | both_nan | (g == r)))
+        return ok, int((d > 0).sum()), float(np.nan_to_num(d, nan=0.0).max(initial=0.0))
     d = np.abs(got.astype(np.int64) - ref.astype(np.int64))
     return bool(d.max(initial=0) <= 1), int((d > 0).sum()), float(d.max(initial=0))
+
+
+def contract_report(got: np.ndarray, ref: np.ndarray, fmt: int) -> dict:
+    """Max LSB (ints) or max abs / max relative error (f32), and the count of
+    differing voxels — printed by the at-size parity tests."""
+    if fmt == 3:
+        g, r = got.astype(np.float64), ref.astype(np.float64)
+        d = np.abs(g - r)
+        rel = d / np.maximum(np.abs(r), np.finfo(np.float64).tiny)
+        return {"n": int(d.size), "ndiff": int((d > 0).sum()), "max_abs": float(d.max(initial=0.0)),
+                "max_rel": float(rel[r != 0].max(initial=0.0))}
+    d = np.abs(got.astype(np.int64) - ref.astype(np.int64))
+    return {"n": int(d.size), "ndiff": int((d > 0).sum()), "max_lsb": int(d.max(initial=0))}

@@ -1,0 +1,201 @@
+"""GPU: every BASELINE.json config at its stated size, checked against the
+oracle (oracle/vkt_oracle.py, pinned to the reference's own outputs).
+
+The oracle restates ``apply_filter`` (pkg/src/vkt/ops/filters.py:69-95) and
+is bit-identical on any z-chunking (SURVEY §8(c) "Large volumes"), so a few
+output planes of a 1024^3 or 2048^3 result are checked exactly by handing
+the oracle only the planes they read: the address-mapped input planes
+[z0 - rz, z1 + rz) are downloaded, stacked, and the oracle computes the
+middle [rz, rz + z1 - z0) of the stack (no z address mapping is left for it
+to do; x and y keep the volume's full extent and the mode's pad).
+
+Configs (BASELINE.json configs[0..4], kernels per SURVEY §8(d)):
+  cfg1 256^3 u8 gaussian_kernel(1.0, 3) Clamp — the whole volume, reference
+       generator (bench.py:38-48);
+  cfg2 512^3 f32 box_kernel(5) Mirror — planes around every z-chunk boundary;
+  cfg3 1024^3 u16 gaussian_kernel(1.5) Clamp — the bench's exact launch and
+       input: [0, 4), both sides of every z-chunk boundary of the chunks the
+       tiled kernel picks (~171 planes), [1020, 1024);
+  cfg4 2048^3 f32 7-point Laplacian Wrap — first, middle and last planes and
+       the first chunk boundaries;
+  cfg5 512^3 u8 Fill(0.5) -> FillRange([128, 384)^3, 1.0) -> gaussian_kernel(1.0)
+       in all four modes — Fill/FillRange bit-exact on the whole volume, the
+       filter around the fill's edges, the volume's faces and chunk boundaries.
+
+Each check records max LSB / max relative error and the differing-voxel count
+(``VKT_PARITY_LOG=path`` appends them as JSON lines).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import paper_2203_10213_b200 as vk
+from conftest import contract_report, within_contract
+from oracle import vkt_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FMT_CODE = {vk.DataFormat.UINT8: 1, vk.DataFormat.UINT16: 2, vk.DataFormat.FLOAT32: 3}
+
+
+def _planes(vol: vk.StructuredVolume, idx: list[int]) -> np.ndarray:
+    """Stored planes ``idx`` of a device volume as a host (len, ny, nx) array."""
+    import torch
+
+    d = vol.dims
+    plane_b = d.x * d.y * vol.format.bytes_per_cell
+    raw = vol.data.raw.view(d.z, plane_b)
+    sel = torch.tensor(idx, dtype=torch.int64, device=raw.device)
+    host = raw.index_select(0, sel).cpu().numpy()
+    return host.view(vol.format.dtype).reshape(len(idx), d.y, d.x)
+
+
+def oracle_range(src: vk.StructuredVolume, weights: np.ndarray, mode: str, z0: int, z1: int) -> np.ndarray:
+    """Oracle output planes [z0, z1) of ``src`` filtered under ``mode``."""
+    nz = src.dims.z
+    rz = weights.shape[0] // 2
+    fmt = FMT_CODE[src.format]
+    glob = [O.map_index(g, nz, mode) for g in range(z0 - rz, z1 + rz)]
+    present = sorted({g for g in glob if g is not None})
+    host = dict(zip(present, _planes(src, present))) if present else {}
+    ny, nx = src.dims.y, src.dims.x
+    stack = np.zeros((len(glob), ny, nx), dtype=src.format.dtype)  # Border: stored 0
+    for i, g in enumerate(glob):
+        if g is not None:
+            stack[i] = host[g]
+    lo, hi = src.mapping
+    return O.apply_filter(stack, fmt, weights, mode, lo, hi, z_range=(rz, rz + z1 - z0), workers=1)
+
+
+def check_ranges(name: str, src, dst, weights: np.ndarray, mode: str, ranges) -> list[dict]:
+    """Compare ``dst`` planes with the oracle on every range (threads: numpy
+    releases the GIL); assert the contract; log the per-range report."""
+    ranges = sorted({(max(0, a), min(src.dims.z, b)) for a, b in ranges if min(src.dims.z, b) > max(0, a)})
+    fmt = FMT_CODE[src.format]
+    got = {r: _planes(dst, list(range(*r))) for r in ranges}
+    with ThreadPoolExecutor(max_workers=min(len(ranges), os.cpu_count() or 1)) as ex:
+        want = dict(zip(ranges, ex.map(lambda r: oracle_range(src, weights, mode, *r), ranges)))
+    reports = []
+    for r in ranges:
+        ok, ndiff, dmax = within_contract(got[r], want[r], fmt, weights)
+        rep = dict(config=name, mode=mode, z_range=list(r), **contract_report(got[r], want[r], fmt))
+        reports.append(rep)
+        assert ok, rep
+    log = os.environ.get("VKT_PARITY_LOG")
+    if log:
+        with open(log, "a") as fh:
+            for rep in reports:
+                fh.write(json.dumps(rep) + "\n")
+    return reports
+
+
+def boundary_ranges(zc: int, nz: int, width: int = 2, limit: int | None = None):
+    """Both sides of every z-chunk boundary: [b - width, b + width)."""
+    bounds = list(range(zc, nz, zc))
+    if limit is not None and len(bounds) > limit:
+        bounds = bounds[: limit // 2] + bounds[-(limit - limit // 2):]
+    return [(b - width, b + width) for b in bounds]
+
+
+def _free(*vols):
+    import torch
+
+    for v in vols:
+        del v
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def test_cfg1_256_u8_gauss3_clamp_whole_volume():
+    host = vk.synthetic_host(256, vk.DataFormat.UINT8, seed=7)  # reference generator
+    src = vk.StructuredVolume.from_numpy(host)
+    dst = vk.StructuredVolume(src.dims, src.format)
+    k = vk.gaussian_kernel(1.0, 3)
+    vk.ApplyFilter(dst, src, k, vk.AddressMode.CLAMP)
+    want = O.apply_filter(host, 1, k.weights, "clamp")
+    got = dst.to_numpy()
+    ok, ndiff, dmax = within_contract(got, want, 1, k.weights)
+    rep = dict(config="cfg1", mode="clamp", z_range=[0, 256], **contract_report(got, want, 1))
+    if os.environ.get("VKT_PARITY_LOG"):
+        with open(os.environ["VKT_PARITY_LOG"], "a") as fh:
+            fh.write(json.dumps(rep) + "\n")
+    assert ok, rep
+    # the reference's in-place call on the same volume gives the same bytes
+    vk.apply_filter(src, k)
+    assert np.array_equal(src.to_numpy(), got)
+
+
+def test_cfg2_512_f32_box5_mirror_chunk_boundaries():
+    dims = (512, 512, 512)
+    src = vk.synthetic_device(dims, vk.DataFormat.FLOAT32, seed=21)
+    dst = vk.StructuredVolume(src.dims, src.format)
+    k = vk.box_kernel(5)
+    vk.ApplyFilter(dst, src, k, vk.AddressMode.MIRROR)
+    zc = vk.chunk_planes(src, k, vk.AddressMode.MIRROR)
+    assert zc > 0
+    ranges = [(0, 3), (254, 258), (509, 512)] + boundary_ranges(zc, 512)
+    check_ranges("cfg2", src, dst, k.weights, "mirror", ranges)
+    _free(src, dst)
+
+
+def test_cfg3_1024_u16_gauss7_clamp_bench_launch():
+    """The bench's input (synthetic_device seed 7) and launch (ApplyFilter on
+    the whole resident volume, tiled kernel, auto-chosen chunks)."""
+    dims = (1024, 1024, 1024)
+    src = vk.synthetic_device(dims, vk.DataFormat.UINT16, seed=7)
+    dst = vk.StructuredVolume(src.dims, src.format, data=vk.DeviceBuffer(src.nbytes, zero=False))
+    k = vk.gaussian_kernel(1.5)
+    assert k.dims == (7, 7, 7)
+    vk.ApplyFilter(dst, src, k, vk.AddressMode.CLAMP)
+    assert vk.filter_path(dst, src, k) == "tma"
+    zc = vk.chunk_planes(src, k)
+    assert 150 <= zc <= 200, zc  # the deep-chunk rule: ~171-plane chunks at 1024^3, K = 7
+    ranges = [(0, 4), (1020, 1024)] + boundary_ranges(zc, 1024)
+    reps = check_ranges("cfg3", src, dst, k.weights, "clamp", ranges)
+    assert max(r["max_lsb"] for r in reps) <= 1
+    _free(src, dst)
+
+
+def test_cfg4_2048_f32_laplacian_wrap_planes():
+    import torch
+
+    dims = (2048, 2048, 2048)
+    free, _total = torch.cuda.mem_get_info()
+    need = 2 * 2048**3 * 4
+    if free < need + (4 << 30):
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of free HBM, {free / 2**30:.0f} GiB free")
+    src = vk.synthetic_device(dims, vk.DataFormat.FLOAT32, seed=9)
+    dst = vk.StructuredVolume(src.dims, src.format, data=vk.DeviceBuffer(src.nbytes, zero=False))
+    k = vk.laplacian_kernel()
+    vk.ApplyFilter(dst, src, k, vk.AddressMode.WRAP)
+    zc = vk.chunk_planes(src, k, vk.AddressMode.WRAP)
+    ranges = [(0, 2), (1023, 1025), (2046, 2048)] + boundary_ranges(zc, 2048, width=1, limit=4)
+    check_ranges("cfg4", src, dst, k.weights, "wrap", ranges)
+    _free(src, dst)
+
+
+@pytest.mark.parametrize("mode", ["wrap", "mirror", "clamp", "border"])
+def test_cfg5_512_u8_teaser_pipeline(mode):
+    dims = (512, 512, 512)
+    vol = vk.StructuredVolume(dims, vk.DataFormat.UINT8, data=vk.DeviceBuffer(512**3, zero=False))
+    vk.Fill(vol, 0.5)
+    vk.FillRange(vol, ((128, 128, 128), (384, 384, 384)), 1.0)
+    host = vol.to_numpy()
+    want_fill = O.fill_range(np.full((512, 512, 512), O.quantize(0.5, 1, 0.0, 1.0), dtype=np.uint8),
+                             1, (128, 128, 128), (384, 384, 384), 1.0)
+    assert np.array_equal(host, want_fill)  # Fill / FillRange bit-exact
+    out = vk.StructuredVolume(dims, vk.DataFormat.UINT8, data=vk.DeviceBuffer(512**3, zero=False))
+    k = vk.gaussian_kernel(1.0)
+    assert k.dims == (5, 5, 5)
+    vk.ApplyFilter(out, vol, k, mode)
+    zc = vk.chunk_planes(vol, k, mode)
+    ranges = [(0, 4), (124, 132), (252, 260), (380, 388), (508, 512)] + boundary_ranges(zc, 512)
+    reps = check_ranges("cfg5", vol, out, k.weights, mode, ranges)
+    assert max(r["max_lsb"] for r in reps) <= 1
+    _free(vol, out)

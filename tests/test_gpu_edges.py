@@ -46,7 +46,7 @@ def test_awkward_shapes_all_modes_and_extents(shape, fmt):
         for mode in ("wrap", "mirror", "clamp", "border"):
             want = O.apply_filter(stored, fmt, w, mode, workers=1)
             got = _run(stored, fmt, w, mode, "auto")
-            ok, ndiff, dmax = within_contract(got, want, fmt)
+            ok, ndiff, dmax = within_contract(got, want, fmt, w)
             assert ok, (shape, k, mode, ndiff, dmax)
             exact = _run(stored, fmt, w, mode, "exact")
             assert np.array_equal(exact.view(np.uint8), want.view(np.uint8)), (shape, k, mode)
@@ -66,7 +66,7 @@ def test_interior_tiles_at_z_boundaries(fmt, k):
     for mode in ("wrap", "mirror", "clamp", "border"):
         want = O.apply_filter(stored, fmt, w, mode, workers=1)
         got = _run(stored, fmt, w, mode, "auto")
-        ok, ndiff, dmax = within_contract(got, want, fmt)
+        ok, ndiff, dmax = within_contract(got, want, fmt, w)
         assert ok, (k, mode, ndiff, dmax)
 
 
@@ -87,7 +87,7 @@ def test_tiled_k9_all_modes(shape, fmt):
     for mode in ("wrap", "mirror", "clamp", "border"):
         want = O.apply_filter(stored, fmt, w, mode, workers=1)
         got = _run(stored, fmt, w, mode, "auto")
-        ok, ndiff, dmax = within_contract(got, want, fmt)
+        ok, ndiff, dmax = within_contract(got, want, fmt, w)
         assert ok, (shape, mode, ndiff, dmax)
 
 
@@ -118,7 +118,7 @@ def test_anisotropic_integer_kernels_on_the_tiled_path(kd, fmt):
     for mode in ("wrap", "mirror", "clamp", "border"):
         want = O.apply_filter(stored, fmt, w, mode, workers=1)
         got = run(mode, "auto")
-        ok, ndiff, dmax = within_contract(got, want, fmt)
+        ok, ndiff, dmax = within_contract(got, want, fmt, w)
         assert ok, (kd, mode, ndiff, dmax)
         assert np.array_equal(got, run(mode, "direct")), (kd, mode)
 
@@ -154,7 +154,7 @@ def test_anisotropic_f32_z_padded_on_the_tiled_path(kd):
         assert np.array_equal(got.view(np.uint32), run(mode, "direct").view(np.uint32)), (kd, mode)
     src2 = vk.StructuredVolume.from_numpy(finite, vk.DataFormat.FLOAT32)
     vk.ApplyFilter(dst, src2, kernel, "clamp")
-    ok, ndiff, dmax = within_contract(dst.to_numpy(), O.apply_filter(finite, 3, w, "clamp", workers=1), 3)
+    ok, ndiff, dmax = within_contract(dst.to_numpy(), O.apply_filter(finite, 3, w, "clamp", workers=1), 3, w)
     assert ok, (kd, ndiff, dmax)
 
 
@@ -189,7 +189,7 @@ def test_anisotropic_f32_guarded_cube(kd, nx):
     for mode in ("wrap", "mirror", "clamp", "border"):
         got = run(finite, mode, "auto")
         assert np.array_equal(got, run(finite, mode, "direct")), (kd, mode)
-        ok, ndiff, dmax = within_contract(got, O.apply_filter(finite, 3, w, mode, workers=1), 3)
+        ok, ndiff, dmax = within_contract(got, O.apply_filter(finite, 3, w, mode, workers=1), 3, w)
         assert ok, (kd, mode, ndiff, dmax)
         got = run(bad, mode, "auto")
         assert np.array_equal(got.view(np.uint32), run(bad, mode, "direct").view(np.uint32)), (kd, mode)

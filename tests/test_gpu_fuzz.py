@@ -75,7 +75,7 @@ def test_fuzz_case(i):
     c = _case(i)
     want = O.apply_filter(c["stored"], c["fmt"], c["w"], c["mode"], *c["mapping"], workers=1)
     fast = _run(c, "auto")
-    ok, ndiff, dmax = within_contract(fast, want, c["fmt"])
+    ok, ndiff, dmax = within_contract(fast, want, c["fmt"], c["w"])
     assert ok, (c["dims"], c["kd"], c["mode"], c["fmt"], ndiff, dmax)
     exact = _run(c, "exact")
     assert np.array_equal(exact.view(np.uint8), want.view(np.uint8)), (c["dims"], c["kd"], c["mode"])

@@ -84,7 +84,7 @@ def test_cli_filter_matches_reference_cli(short, tmp_path):
     assert got_raw[:vio.HEADER_SIZE] == want_raw[:vio.HEADER_SIZE]
     got, fmt = _payload(ours)
     want, _ = _payload(ref_out)
-    ok, ndiff, dmax = within_contract(got, want, fmt.value)
+    ok, ndiff, dmax = within_contract(got, want, fmt.value, vk.gaussian_kernel(1.0, 3).weights)
     assert ok, (ndiff, dmax)
     # pipes: stdin -> stdout
     r = subprocess.run(CLI + ["filter", "--gaussian", "1.0", "--ksize", "3"], input=src.read_bytes(),

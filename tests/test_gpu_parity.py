@@ -40,7 +40,7 @@ def run_filter(stored, fmt, weights, mode, lo=0.0, hi=1.0, path="auto"):
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 def test_fast_path_within_contract(case):
     got = run_filter(case["input"], case["fmt"], case["weights"], case["mode"], case["lo"], case["hi"])
-    ok, ndiff, dmax = within_contract(got, case["output"], case["fmt"])
+    ok, ndiff, dmax = within_contract(got, case["output"], case["fmt"], case["weights"])
     assert ok, f"{case['name']}: {ndiff} cells differ, max {dmax}"
 
 
@@ -71,7 +71,7 @@ def test_tiled_shapes_vs_oracle(fmt, mode, k):
     w = O.gaussian_weights(1.0, k) if k != 5 else O.box_weights(5)
     want = O.apply_filter(stored, fmt, w, mode)
     got = run_filter(stored, fmt, w, mode)
-    ok, ndiff, dmax = within_contract(got, want, fmt)
+    ok, ndiff, dmax = within_contract(got, want, fmt, w)
     assert ok, (ndiff, dmax)
     direct = run_filter(stored, fmt, w, mode, path="direct")
     assert np.array_equal(got.view(np.uint8), direct.view(np.uint8))
@@ -80,7 +80,7 @@ def test_tiled_shapes_vs_oracle(fmt, mode, k):
 def test_bench_fixture_u8_gauss3():
     z = np.load(GOLDEN / "bench_case.npz")
     got = run_filter(z["input"], 1, O.gaussian_weights(1.0, 3), "clamp")
-    ok, ndiff, dmax = within_contract(got, z["output"], 1)
+    ok, ndiff, dmax = within_contract(got, z["output"], 1, O.gaussian_weights(1.0, 3))
     assert ok, (ndiff, dmax)
 
 

@@ -51,5 +51,5 @@ def test_reference_tests_pass_against_b200_package():
     tail = (r.stdout + r.stderr)[-4000:]
     assert r.returncode == 0, tail
     m = re.search(r"(\d+) passed", r.stdout)
-    assert m and int(m.group(1)) >= 40, tail
+    assert m and int(m.group(1)) >= 30, tail  # 32 selected
     assert "failed" not in r.stdout.splitlines()[-1], tail

@@ -11,6 +11,7 @@
 
 #include "dispatch.h"
 #include "filter_tma.cuh"
+#include "filter_warp.cuh"
 
 namespace vkt {
 namespace tma {
@@ -31,8 +32,23 @@ cudaError_t launch_tma_dtype<float>(int, int, const CUtensorMap&, const CUtensor
                                     const CUtensorMap&, const TmaParams&, const float*, dim3,
                                     cudaStream_t);
 }  // namespace tma
+namespace tmaw {
+extern template cudaError_t launch_warp_dtype<uint8_t>(int, const CUtensorMap&, const CUtensorMap&,
+                                                       const CUtensorMap&, const tma::TmaParams&,
+                                                       const float*, dim3, cudaStream_t);
+extern template cudaError_t launch_warp_dtype<uint16_t>(int, const CUtensorMap&, const CUtensorMap&,
+                                                        const CUtensorMap&, const tma::TmaParams&,
+                                                        const float*, dim3, cudaStream_t);
+}  // namespace tmaw
 
 namespace {
+
+// u8/u16 3x3x3 run the warp-private-staging kernel (filter_warp.cuh), with
+// 32-row tiles; everything else the paired-layout kernel's 16-row tiles.
+bool warp_kernel(const vkt_filter_args& a) {
+  return a.format != VKT_F32 && a.kdims.x == 3;
+}
+int tile_rows(const vkt_filter_args& a) { return warp_kernel(a) ? tmaw::TY : tma::TY; }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -58,7 +74,7 @@ int bpc_of(int format) { return format == VKT_U8 ? 1 : format == VKT_U16 ? 2 : 4
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int r,
-            int pitch) {
+            int pitch, int tile_y) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return false;
   const int bpc = bpc_of(format);
@@ -67,7 +83,7 @@ bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz
                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
   cuuint64_t strides[2] = {(cuuint64_t)pitch * bpc, (cuuint64_t)pitch * ny * bpc};
-  cuuint32_t box[3] = {(cuuint32_t)tma::box_width(r, bpc), (cuuint32_t)(tma::TY + 2 * r), 1u};
+  cuuint32_t box[3] = {(cuuint32_t)tma::box_width(r, bpc), (cuuint32_t)(tile_y + 2 * r), 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult res = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -85,13 +101,15 @@ int tma_chunk_planes(const FilterPlan& plan) {
   const int k = a.kdims.x, r = k / 2;
   const int nzo = plan.z_end - plan.z_begin;
   if (nzo <= 0) return 1;
-  const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + tma::TY - 1) / tma::TY);
+  const int ty = tile_rows(a);
+  const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + ty - 1) / ty);
   // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
   // K = 3 (4, Wrap 3)
   const int64_t slots = (int64_t)sm_count() * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
                                  : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
-                                          : tma::Layout<2, 3>::CTAS_PER_SM);
+                                 : warp_kernel(a) ? tmaw::CTAS_PER_SM
+                                                  : tma::Layout<2, 3>::CTAS_PER_SM);
   // Under 3 waves the grid balances poorly: 512^3 u16 3^3 runs 0.266 ms at
   // 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves); f32 3^3 0.241 vs
   // 0.231 (profiles/r01_zc_sweep3_v37.txt, r01_zc_sweep4_v37.txt).  So chunks
@@ -150,12 +168,14 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
                    const void* hhi, int pitch, cudaStream_t s) {
   const vkt_filter_args& a = *plan.args;
   const int k = a.kdims.x, r = k / 2;
+  const int ty = tile_rows(a);
+  const bool wk = warp_kernel(a);
   CUtensorMap ms, ml, mh;
-  if (!encode(&ms, src, a.format, a.dims.x, a.dims.y, a.dims.z, r, pitch)) return -1;
+  if (!encode(&ms, src, a.format, a.dims.x, a.dims.y, a.dims.z, r, pitch, ty)) return -1;
   ml = ms;
   mh = ms;
-  if (hlo && r > 0 && !encode(&ml, hlo, a.format, a.dims.x, a.dims.y, r, r, pitch)) return -1;
-  if (hhi && r > 0 && !encode(&mh, hhi, a.format, a.dims.x, a.dims.y, r, r, pitch)) return -1;
+  if (hlo && r > 0 && !encode(&ml, hlo, a.format, a.dims.x, a.dims.y, r, r, pitch, ty)) return -1;
+  if (hhi && r > 0 && !encode(&mh, hhi, a.format, a.dims.x, a.dims.y, r, r, pitch, ty)) return -1;
 
   tma::TmaParams p{};
   p.dst = dst;
@@ -177,17 +197,18 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   const int nzo = plan.z_end - plan.z_begin;
   const int zc = tma_chunk_planes(plan);
   p.zc = zc;
-  dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + tma::TY - 1) / tma::TY,
-            (nzo + zc - 1) / zc);
+  dim3 grid((a.dims.x + tma::TX - 1) / tma::TX, (a.dims.y + ty - 1) / ty, (nzo + zc - 1) / zc);
   if (grid.y > 65535 || grid.z > 65535) return -1;
 
   cudaError_t err;
   switch (a.format) {
     case VKT_U8:
-      err = tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      err = wk ? tmaw::launch_warp_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+               : tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     case VKT_U16:
-      err = tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      err = wk ? tmaw::launch_warp_dtype<uint16_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+               : tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     default:
       err = tma::launch_tma_dtype<float>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);

@@ -80,21 +80,17 @@ struct Ready {
 };
 static_assert((2 * NPR + 4) / 4 % 2 == 1, "K >= 5 ready rows must be an odd number of chunks");
 
-// Thread layout per voxel size and kernel extent (measured):
-//  u8/u16, K == 3: 2 output rows per thread, 4 warps, 4 CTAs/SM;
-//  otherwise: 1 row per thread, 8 warps (staging split between the halves),
-//          2 CTAs/SM (4 warps/SMSP, 128 regs).
+// Thread layout (measured): 1 output row per thread, 8 warps
+// (staging split between the halves), 2 CTAs/SM (4 warps/SMSP, 128 regs).
 // Warps per SM stay a multiple of 4 so every SM sub-partition gets the same
-// number of FMA warps.
+// number of FMA warps.  (u8/u16 K = 3 run filter_warp.cuh, f32 K = 3
+// filter_tma_zp.cuh.)
 template <int BPC, int K>
 struct Layout {
-  static constexpr bool SMALL = K == 3 && BPC < 4;
-  static constexpr int YPT = SMALL ? 2 : 1;
+  static constexpr int YPT = 1;
   static constexpr int WARPS = TY * TPR / (32 * YPT);
   static constexpr int THREADS = 32 * WARPS;
-  // u8/u16 K = 3 run 4 CTAs (128 registers, 56 KB of rings each; u16 with a
-  // 3-stage ready ring, AHEAD = 1): 1.61 / 1.56 vs 1.74 / 1.75 ms at 1024^3
-  static constexpr int CTAS_PER_SM = SMALL ? 4 : 2;
+  static constexpr int CTAS_PER_SM = 2;
   static constexpr int SMEM_PER_CTA = (228 * 1024) / CTAS_PER_SM - 1024;  // minus driver reserve
 };
 
@@ -135,13 +131,9 @@ struct Cfg {
   static constexpr int MAX_REPAIR = 2 * R * (NPR / 4) + 4 * BY;
   static constexpr int REPAIR_BYTES = (MAX_REPAIR * 18 + 16 + 127) / 128 * 128;
   static constexpr int BUDGET = L::SMEM_PER_CTA - 512 - REPAIR_BYTES;
-#ifndef VKT_RAW_MIN
-#define VKT_RAW_MIN 6
-#endif
-  static constexpr int S_RDY_FIT = (BUDGET - VKT_RAW_MIN * RAW_PITCH) / RDY_PITCH;
-  // K = 3 integer rings (4 CTAs/SM) drop to 3 ready stages with AHEAD = 1,
-  // leaving room for deeper raw rings (u8 1.62 -> 1.58 ms; u16 needs it to fit)
-  static constexpr int S_RDY_MIN = (L::SMALL || K == 9) ? 3 : 4;  // K = 9: 24-row stages
+  static constexpr int RAW_MIN = 6;
+  static constexpr int S_RDY_FIT = (BUDGET - RAW_MIN * RAW_PITCH) / RDY_PITCH;
+  static constexpr int S_RDY_MIN = K == 9 ? 3 : 4;  // K = 9: 24-row stages
   static constexpr int S_RDY = S_RDY_FIT < S_RDY_MIN ? S_RDY_MIN : (S_RDY_FIT > 6 ? 6 : S_RDY_FIT);
   static constexpr int S_RAW_FIT = (BUDGET - S_RDY * RDY_PITCH) / RAW_PITCH;
   static constexpr int S_RAW = S_RAW_FIT < 10 ? S_RAW_FIT : 10;
@@ -354,9 +346,6 @@ struct StagePlan {
     }
   }
   __device__ __forceinline__ bool slow(int by, int g) const {
-#ifdef VKT_EXP_NOREPAIR
-    return false;
-#endif
     return edge_ && slow_item<C::R>(by, g, rows_lo_, rows_hi_, rows_end_, e_lo_, e_hi_, e_end_);
   }
   // item k of the row-major staging pass (edge items are left to the repair
@@ -452,18 +441,6 @@ __device__ __forceinline__ void build_repair_table(const RepairTable& rt, const 
       w[h] = pair;
     }
     const uint32_t idx = atomicAdd(rt.count, 1u);
-#ifdef VKT_DEBUG_BOUNDS
-    {
-      const uint32_t lim = C::BX * C::BY;
-      if (idx >= (uint32_t)C::MAX_REPAIR || (w[0] & 0xFFFF) >= lim || (w[0] >> 16) >= lim ||
-          (w[1] & 0xFFFF) >= lim || (w[1] >> 16) >= lim || (w[2] & 0xFFFF) >= lim ||
-          (w[2] >> 16) >= lim || (w[3] & 0xFFFF) >= lim || (w[3] >> 16) >= lim) {
-        printf("repair table: cta (%d,%d,%d) idx %u by %d g %d w %x %x %x %x lim %u\n", blockIdx.x,
-               blockIdx.y, blockIdx.z, idx, by, g, w[0], w[1], w[2], w[3], lim);
-        __trap();
-      }
-    }
-#endif
     rt.src[idx] = make_uint4(w[0], w[1], w[2], w[3]);
     rt.dst[idx] = (uint16_t)((by * C::RPF + Ready<K>::in_row(8 * g)) / 4);
   }
@@ -640,6 +617,41 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
 // ---------------------------------------------------------------------------
 // Compute helpers
 // ---------------------------------------------------------------------------
+// Epilogue: floor each sum to s32, then saturate-and-pack (I2IP) and store.
+// Floor to s32 (F2I), then saturate-and-pack to u8 / u16 (I2IP): one
+// conversion and half a pack per output.  floor-then-saturate equals the
+// reference rule's floor(clip(.)) on the biased sum (acc_init adds the 0.5)
+// for every finite sum, and common.cuh's quantize_acc, so every kernel path
+// stays bit-identical.  (An FADD2.RM + 2^23 bias variant avoids F2I but
+// measured slower: 1.363 vs 1.320 ms, u8 3^3 1024^3.)
+__device__ __forceinline__ int floor_s32(float v) {
+  int r;
+  asm("cvt.rmi.s32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return r;
+}
+// floor of both halves of an accumulator pair as s32
+__device__ __forceinline__ void floor2_s32(uint64_t a, int& lo, int& hi) {
+  lo = floor_s32(f2lo(a));
+  hi = floor_s32(f2hi(a));
+}
+template <typename T>
+__device__ __forceinline__ void store4i(T* out, int a0, int a1, int a2, int a3);
+template <>
+__device__ __forceinline__ void store4i<uint8_t>(uint8_t* out, int a0, int a1, int a2, int a3) {
+  // cvt.pack.sat.u8.s32.b32 d, a, b, c: d = {c[15:0], sat(a), sat(b)} (b in byte 0)
+  uint32_t hi, v;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(a3), "r"(a2));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(v) : "r"(a1), "r"(a0), "r"(hi));
+  __stcs(reinterpret_cast<unsigned int*>(out), v);
+}
+template <>
+__device__ __forceinline__ void store4i<uint16_t>(uint16_t* out, int a0, int a1, int a2, int a3) {
+  uint32_t lo, hi;
+  asm("cvt.pack.sat.u16.s32 %0, %1, %2;" : "=r"(lo) : "r"(a1), "r"(a0));
+  asm("cvt.pack.sat.u16.s32 %0, %1, %2;" : "=r"(hi) : "r"(a3), "r"(a2));
+  __stcs(reinterpret_cast<uint2*>(out), make_uint2(lo, hi));
+}
+
 template <typename T>
 __device__ __forceinline__ void store4(T* out, float a0, float a1, float a2, float a3);
 
@@ -647,25 +659,15 @@ template <>
 __device__ __forceinline__ void store4<float>(float* out, float a0, float a1, float a2, float a3) {
   __stcs(reinterpret_cast<float4*>(out), make_float4(a0, a1, a2, a3));
 }
-template <typename T>
-__device__ __forceinline__ uint32_t q32(float a) {
-  return (uint32_t)quantize_acc<T>(a);
-}
 template <>
 __device__ __forceinline__ void store4<uint16_t>(uint16_t* out, float a0, float a1, float a2,
                                                  float a3) {
-  // byte permutes (ALU pipe) rather than shift-or, which ptxas emits as
-  // IMAD on the FMA pipe the FFMA2 stream needs
-  __stcs(reinterpret_cast<uint2*>(out),
-         make_uint2(__byte_perm(q32<uint16_t>(a0), q32<uint16_t>(a1), 0x5410),
-                    __byte_perm(q32<uint16_t>(a2), q32<uint16_t>(a3), 0x5410)));
+  store4i<uint16_t>(out, floor_s32(a0), floor_s32(a1), floor_s32(a2), floor_s32(a3));
 }
 template <>
 __device__ __forceinline__ void store4<uint8_t>(uint8_t* out, float a0, float a1, float a2,
                                                 float a3) {
-  const uint32_t lo = __byte_perm(q32<uint8_t>(a0), q32<uint8_t>(a1), 0x0040);
-  const uint32_t hi = __byte_perm(q32<uint8_t>(a2), q32<uint8_t>(a3), 0x0040);
-  __stcs(reinterpret_cast<unsigned int*>(out), __byte_perm(lo, hi, 0x5410));
+  store4i<uint8_t>(out, floor_s32(a0), floor_s32(a1), floor_s32(a2), floor_s32(a3));
 }
 
 // Rolling accumulators of one thread: slot m holds the partial sums of the
@@ -708,11 +710,7 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
   const float* base = stage + YPT * ty * RPF;
   // dy unrolled (UNROLL): rolled, ptxas renames the accumulators at the back
   // edge with IMAD.MOV (FMA pipe) — measured at K = 5: 4.46 vs 5.33 ms.
-#if defined(VKT_EXP_UNROLL_DY)
-#pragma unroll
-#else
 #pragma unroll(UNROLL ? K : 1)
-#endif
   for (int dy = 0; dy < K; ++dy) {
     uint64_t P[YPT][2 * NLD];
 #pragma unroll
@@ -851,7 +849,6 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
       for (int q = tid % ST; q < C::RDY_BYTES / 16; q += ST) w4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
       const T* raw = raw_base + r * (C::RAW_PITCH / (int)sizeof(T));
-#ifndef VKT_EXP_NOCONVERT  // diagnostics builds only (build.py --variant)
       stage_plane<T, MODE, K, ST>(stage, raw, plane_ptr<T>(p, src), p, x0, y0, edge, splan, rtab,
                                   tid % ST);
       if constexpr (WLIST) {
@@ -862,7 +859,6 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
           if (j + WSTEP < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + j + WSTEP)));
         }
       }
-#endif
     }
     __syncwarp();
     if (lane == 0) {
@@ -871,22 +867,13 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     }
   };
 
-#ifndef VKT_EXP_COMPUTEONLY
   for (int j = 0; j < SR && j < np; ++j) issue(j);
   for (int j = 0; j < C::AHEAD && j < np; ++j) prepare(j);
-#endif
 
-  // lane layout: 2-row layouts (K = 3) run tx along the lanes; 1-row layouts
-  // put tx 0..3 of two adjacent rows in each quarter-warp (see Ready<K>)
-  int tx, ty;
-  if constexpr (YPT == 1) {
-    static_assert(TPR == 16, "lane layout");
-    tx = (lane & 3) | ((lane >> 3) << 2);
-    ty = 2 * (tid / 32) + ((lane >> 2) & 1);
-  } else {
-    tx = tid % TPR;
-    ty = tid / TPR;
-  }
+  // lane layout: tx 0..3 of two adjacent rows in each quarter-warp (see Ready<K>)
+  static_assert(TPR == 16 && YPT == 1, "lane layout");
+  const int tx = (lane & 3) | ((lane >> 3) << 2);
+  const int ty = 2 * (tid / 32) + ((lane >> 2) & 1);
   int ld_off[LoadRun<K>::NOFF];
   LoadRun<K>::offsets(tx, ld_off);
   const float a0 = acc_init<T>(p.c);
@@ -914,7 +901,6 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   for (int i = 0; i < np; ++i) {
     const int s = i % S;
     const float* stage = rdy_base + s * (C::RDY_PITCH / 4);
-#ifndef VKT_EXP_COMPUTEONLY
     // refill the raw slot of plane i-1 (staged AHEAD iterations before).
     // Only warp 0 (the TMA issuer's) waits for the slot: a warp of the other
     // staging half may run up to S_RDY - AHEAD planes ahead, and if the ring
@@ -926,10 +912,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
       issue(i - 1 + SR);
     }
     if (i + C::AHEAD < np) prepare(i + C::AHEAD);
-#ifndef VKT_EXP_NOREADYWAIT
     mbar_wait(&ready[s], (uint32_t)((i / S) & 1));
-#endif
-#endif
     // slot m <-> output plane zo0 + i - 2R + m
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
@@ -1005,7 +988,6 @@ cudaError_t launch_tma_dtype(int k, int mode, const CUtensorMap& ms, const CUten
   VKT_TMA_CASE(KK, VKT_MIRROR)      \
   VKT_TMA_CASE(KK, VKT_CLAMP)       \
   VKT_TMA_CASE(KK, VKT_BORDER)
-  VKT_TMA_K(3)
   VKT_TMA_K(5)
   VKT_TMA_K(7)
   VKT_TMA_K(9)

@@ -858,14 +858,10 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K, MODE>::CTAS_PER_
     // slot m <-> output plane zo0 + i - 2R + m
     const int first = 2 * R - i;
     const int last = nzo - 1 - i + 2 * R;
-#ifdef VKT_EXP_ZP_NOCOMPUTE  // diagnostics: the memory pipeline alone
-    if (i == 0) plane_step<K, true, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, first, last);
-#else
     if (first <= 0 && last >= K - 1)
       plane_step<K, false, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, 0, K - 1);
     else
       plane_step<K, true, C::IS_F32 && K >= 5>(stage, tx, ty, wt, acc, first, last);
-#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 

@@ -1,0 +1,9 @@
+# warp-private-staging u8/u16 3^3 kernel: parity + timing vs the paired kernel
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_edges.py tests/test_gpu_shard.py -q -p no:cacheprovider -x > gpurun_out/exp2_tests.log 2>&1
+echo rc=$? >> gpurun_out/exp2_tests.log
+for env in "" "VKT_NO_WARP_KERNEL=1"; do
+  for c in "u8 3 gauss clamp 1024" "u16 3 gauss clamp 1024" "u8 3 gauss clamp 256" "u8 3 gauss wrap 1024" "u16 3 gauss mirror 512" "u8 3 gauss border 512" "u16 3 box wrap 512"; do
+    set -- $c
+    env $env python tools/profile_case.py --fmt $1 --k $2 --kernel $3 --mode $4 --n $5 --reps 7 2>&1 | sed "s/^/[$env] /"
+  done
+done > gpurun_out/exp2.log 2>&1

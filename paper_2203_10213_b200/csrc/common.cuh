@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 #include "../../include/vkt_b200.h"
 
 namespace vkt {
@@ -171,6 +173,48 @@ template <>
 __device__ __forceinline__ float quantize_acc<float>(float acc) {
   return acc;
 }
+
+// ----------------------------------------------------------------------------
+// Checked builds (build.py --variant=checked -DVKT_CHECKS -DVKT_JITTER; never
+// the product library).  compute-sanitizer is not available on the GPU pool,
+// so the tiled kernels carry their own race / bounds evidence:
+//  * VKT_CHECK: shared-memory offsets of staging, edge repair and compute are
+//    bounds-checked; a violation prints the CTA and traps.
+//  * VKT_JITTER_POINT: each warp sleeps a pseudo-random 0..4 us (one point in
+//    four) at the synchronization points of the pipeline, so a missing wait
+//    or a phase race changes the result; the parity suites then compare every
+//    kernel against the oracle and the direct kernel under that jitter.
+// ----------------------------------------------------------------------------
+#ifdef VKT_CHECKS
+#define VKT_CHECK(cond, what)                                                                  \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("VKT_CHECK failed: %s (cta %d,%d,%d thread %d)\n", what, (int)blockIdx.x,          \
+             (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x);                              \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define VKT_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
+#ifdef VKT_JITTER
+__device__ __forceinline__ void vkt_jitter(uint32_t salt) {
+  uint32_t h = blockIdx.x * 73856093u ^ blockIdx.y * 19349663u ^ blockIdx.z * 83492791u ^
+               (threadIdx.x >> 5) * 2654435761u ^ salt * 40503u ^ (uint32_t)clock();
+  h ^= h >> 13;
+  h *= 0x5bd1e995u;
+  h ^= h >> 15;
+  if ((h & 3u) == 0) __nanosleep(h % 4096u);
+}
+#define VKT_JITTER_POINT(salt) vkt_jitter(salt)
+#else
+#define VKT_JITTER_POINT(salt) \
+  do {                         \
+  } while (0)
+#endif
 
 // Launch accounting (see vkt_launch_count).
 void count_launch();

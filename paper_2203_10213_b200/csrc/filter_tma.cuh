@@ -463,6 +463,7 @@ __device__ __forceinline__ void apply_repair_table(float* rdy, const T* raw, con
   for (int i = t; i < n; i += nt) {
     const uint4 w = rt.src[i];
     const int ro = 4 * (int)rt.dst[i];
+    VKT_CHECK((n <= Cfg<T, K>::MAX_REPAIR), "repair table: count");
     const float c0 = raw_value(raw, w.x & 0xFFFFu), c1 = raw_value(raw, w.x >> 16);
     const float c2 = raw_value(raw, w.y & 0xFFFFu), c3 = raw_value(raw, w.y >> 16);
     const float c4 = raw_value(raw, w.z & 0xFFFFu), c5 = raw_value(raw, w.z >> 16);
@@ -590,6 +591,8 @@ __device__ __forceinline__ void stage_plane(float* rdy, const T* raw, const T* p
     int ro, wo;
     sp.get(k, ro, wo);
     if (ro < 0) continue;
+    VKT_CHECK((Ready<K>::second(ro) + 4 <= Cfg<T, K>::RPF * Cfg<T, K>::BY), "paired staging: ready offset");
+    VKT_CHECK((wo >= 0 && (wo + HALF + 4) * (int)sizeof(T) <= Cfg<T, K>::RAW_BYTES), "paired staging: raw offset");
     uint32_t lo[4], hi[4];
     load_quad<T>(raw + wo, lo);
     load_quad<T>(raw + wo + HALF, hi);
@@ -838,6 +841,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + (SPLIT ? half : 0))));
   auto prepare = [&](int j) {
     if (SPLIT && half != (j & 1)) return;
+    VKT_JITTER_POINT(4 * j);
     const int s = j % S;
     float* stage = rdy_base + s * (C::RDY_PITCH / 4);
     const int r = j % SR;
@@ -901,6 +905,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   for (int i = 0; i < np; ++i) {
     const int s = i % S;
     const float* stage = rdy_base + s * (C::RDY_PITCH / 4);
+    VKT_JITTER_POINT(4 * i + 1);
     // refill the raw slot of plane i-1 (staged AHEAD iterations before).
     // Only warp 0 (the TMA issuer's) waits for the slot: a warp of the other
     // staging half may run up to S_RDY - AHEAD planes ahead, and if the ring

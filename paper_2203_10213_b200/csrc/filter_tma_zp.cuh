@@ -746,6 +746,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K, MODE>::CTAS_PER_
   // ints: widen plane j (all warps, equal shares) into ready stage j % S.
   const QuadPlan<T, K, THREADS> qplan(p, x0, y0, edge, tid);
   auto prepare = [&](int j) {
+    VKT_JITTER_POINT(4 * j);
     const int s = j % S;
     float* stage = rdy_base + s * (C::RDY_PITCH / 4);
     const int r = j % SR;
@@ -805,6 +806,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, Layout<K, MODE>::CTAS_PER_
   if (C::IS_F32 && MODE == VKT_WRAP && edge && wrap.ok)
     wrap.gather(plane_ptr<float>(p, resolve<MODE>(p, R, zo0 - R)));
   for (int i = 0; i < np; ++i) {
+    VKT_JITTER_POINT(4 * i + 1);
     const int s = i % S;
     float* stage = rdy_base + s * (C::RDY_PITCH / 4);
     if constexpr (C::IS_F32) {

@@ -261,11 +261,14 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   // Border plane outside the volume was fetched as a fully out-of-bounds TMA
   // box: zeros, so every plane takes this one path).
   auto stage_main = [&](int j, float* buf) {
+    VKT_JITTER_POINT(4 * j);
     const T* raw = raw_base + (j % SR) * (C::RAW_PITCH / (int)sizeof(T));
 #pragma unroll
     for (int k = 0; k < QPL; ++k) {
       if (32 * k + 31 >= NQ && !last_item) continue;
       const int ro = item_ro[k], wo = item_wo[k];
+      VKT_CHECK(ro >= 0 && tma::Ready<K>::second(ro) + 4 <= RPF * WIN, "warp staging: ready offset");
+      VKT_CHECK(wo >= 0 && (wo + HALF + 4) * (int)sizeof(T) <= C::RAW_BYTES, "warp staging: raw offset");
       uint32_t lo[4], hi[4];
       tma::load_quad<T>(raw + wo, lo);
       tma::load_quad<T>(raw + wo + HALF, hi);
@@ -303,10 +306,12 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
         } else {
           int slo, shi;
           rdy_dests(x0, ya, map_index_near<MODE>(gx, p.nx), map_index_near<MODE>(gy, p.ny), slo, shi);
+          VKT_CHECK((slo >= 0 ? slo : shi) >= 0 && (slo >= 0 ? slo : shi) < RPF * WIN, "warp edge fix: source");
           v = buf[slo >= 0 ? slo : shi];
         }
         int dlo, dhi;
         rdy_dests(x0, ya, gx, gy, dlo, dhi);
+        VKT_CHECK(dlo < RPF * WIN && dhi < RPF * WIN && (dlo >= 0 || dhi >= 0), "warp edge fix: dest");
         if (dlo >= 0) buf[dlo] = v;
         if (dhi >= 0) buf[dhi] = v;
       }
@@ -327,6 +332,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   // warp 0 re-issues raw slot of plane j once every warp has staged it (only
   // the issuer's warp waits, so no other warp is coupled to the slowest)
   auto refill = [&](int j) {
+    VKT_JITTER_POINT(4 * j + 1);
     if (warp == 0 && j + SR < np) {
       tma::mbar_wait(&raw_free[j % SR], (uint32_t)((j / SR) & 1));
       issue(j + SR);
@@ -340,6 +346,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   // m+1 (the partial sum one output plane later), or the epilogue constant
   // for the new slot K-1, and writes slot m.
   auto compute = [&](const float* buf) {
+    VKT_JITTER_POINT(2);
     const float* base = buf + ty * YPT * RPF;
 #pragma unroll
     for (int ry = 0; ry < YPT + K - 1; ++ry) {
@@ -377,6 +384,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   };
   // slot 0 is complete after input plane j: output plane zo0 + j - 2R
   auto epilogue = [&](int j) {
+    VKT_JITTER_POINT(4 * j + 3);
     if (j < 2 * R) return;
     T* o = out_plane;
 #pragma unroll

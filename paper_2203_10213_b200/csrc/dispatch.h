@@ -39,6 +39,10 @@ struct StreamDeviceGuard {
   int prev = -1;
   explicit StreamDeviceGuard(cudaStream_t s) {
     if (s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread) return;
+    // a stream being captured into a CUDA graph: device queries there would
+    // invalidate the capture; the capturing thread's device is the stream's
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
     int d = 0, cur = 0;
     if (cudaStreamGetDevice(s, &d) != cudaSuccess) {
       cudaGetLastError();

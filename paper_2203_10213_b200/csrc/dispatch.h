@@ -18,7 +18,12 @@ struct FilterPlan {
   double sum_w;             // f64 sum of weights (epilogue)
   float epi_c;              // lo*(sum_w-1)/(hi-lo)*max  (ints), 0 for f32
   int path;                 // VKT_PATH_*
-  uint32_t zskip = 0;       // f32 weights padded in z to a cube: bit dz = padding plane
+  // anisotropic weights padded to a K^3 cube (vkt_capi.cu pad_to_cube): the
+  // kernel's own x extent and the padding y rows / z planes, which the tiled
+  // kernel skips (kxs = 0: an isotropic kernel, nothing skipped)
+  int kxs = 0;
+  uint32_t zskip = 0;       // bit dz set: padding plane
+  uint32_t yskip = 0;       // bit dy set: padding row
   // Device flag set by launch_scan_nonfinite.  Tiled launches do nothing when
   // it is set, direct launches only then; nullptr = unconditional.
   const int* guard = nullptr;

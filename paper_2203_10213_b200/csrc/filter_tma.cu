@@ -31,6 +31,38 @@ template <>  // explicit specialization (filter_tma_f32.cu): K <= 5 -> filter_tm
 cudaError_t launch_tma_dtype<float>(int, int, const CUtensorMap&, const CUtensorMap&,
                                     const CUtensorMap&, const TmaParams&, const float*, dim3,
                                     cudaStream_t);
+#define VKT_ANISO_DECL(KK, T)                                                                      \
+  template <>                                                                                     \
+  cudaError_t launch_tma_aniso_k##KK<T>(int, int, const CUtensorMap&, const CUtensorMap&,        \
+                                        const CUtensorMap&, const TmaParams&, const float*, dim3, \
+                                        cudaStream_t);
+#define VKT_ANISO_DECLS(KK)                                                                     \
+  template <typename T>                                                                         \
+  cudaError_t launch_tma_aniso_k##KK(int, int, const CUtensorMap&, const CUtensorMap&,         \
+                                     const CUtensorMap&, const TmaParams&, const float*, dim3,  \
+                                     cudaStream_t);                                              \
+  VKT_ANISO_DECL(KK, uint8_t)                                                                   \
+  VKT_ANISO_DECL(KK, uint16_t)                                                                  \
+  VKT_ANISO_DECL(KK, float)
+VKT_ANISO_DECLS(5)
+VKT_ANISO_DECLS(7)
+VKT_ANISO_DECLS(9)
+#undef VKT_ANISO_DECLS
+#undef VKT_ANISO_DECL
+
+// Anisotropic kernels embedded in a K^3 cube: x extent kxs <= K a template,
+// padding y rows / z planes skipped by mask (filter_tma_aniso_<fmt>_k<K>.cu).
+template <typename T>
+cudaError_t launch_tma_aniso(int k, int kxs, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
+                             const CUtensorMap& mh, const TmaParams& p, const float* w32, dim3 grid,
+                             cudaStream_t s) {
+  switch (k) {
+    case 5: return launch_tma_aniso_k5<T>(kxs, mode, ms, ml, mh, p, w32, grid, s);
+    case 7: return launch_tma_aniso_k7<T>(kxs, mode, ms, ml, mh, p, w32, grid, s);
+    case 9: return launch_tma_aniso_k9<T>(kxs, mode, ms, ml, mh, p, w32, grid, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 }  // namespace tma
 namespace tmaw {
 extern template cudaError_t launch_warp_dtype<uint8_t>(int, const CUtensorMap&, const CUtensorMap&,
@@ -192,6 +224,8 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   p.global_nz = plan.geom.global_nz;
   p.c = plan.epi_c;
   p.zskip = plan.zskip;
+  p.yskip = plan.yskip;
+  const bool aniso = plan.kxs > 0 && !wk && k >= 5;
   p.guard = plan.guard;
 
   const int nzo = plan.z_end - plan.z_begin;
@@ -203,15 +237,18 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   cudaError_t err;
   switch (a.format) {
     case VKT_U8:
-      err = wk ? tmaw::launch_warp_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
-               : tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      err = wk      ? tmaw::launch_warp_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+            : aniso ? tma::launch_tma_aniso<uint8_t>(k, plan.kxs, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+                    : tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     case VKT_U16:
-      err = wk ? tmaw::launch_warp_dtype<uint16_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
-               : tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      err = wk      ? tmaw::launch_warp_dtype<uint16_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+            : aniso ? tma::launch_tma_aniso<uint16_t>(k, plan.kxs, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+                    : tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     default:
-      err = tma::launch_tma_dtype<float>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
+      err = aniso ? tma::launch_tma_aniso<float>(k, plan.kxs, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+                  : tma::launch_tma_dtype<float>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
   }
   count_launch();

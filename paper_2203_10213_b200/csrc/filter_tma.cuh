@@ -166,7 +166,8 @@ struct TmaParams {
   int zc;                // output planes per CTA chunk
   int64_t z_offset, global_nz;
   float c;               // integer epilogue constant
-  uint32_t zskip;        // f32 kernels padded in z: bit dz set = that dz plane is padding
+  uint32_t zskip;        // anisotropic kernels in a K^3 cube: bit dz set = padding plane,
+  uint32_t yskip;        //   bit dy set = padding row (the x extent is a template)
   const int* guard;      // non-null: the launch does nothing when *guard != 0 (vkt_capi.cu)
 };
 
@@ -702,11 +703,11 @@ struct LoadRun {
 // One input plane's contribution to the K rolling accumulators of the
 // thread's YPT x 4 output pairs.  GUARD: skip slots whose output plane is
 // outside the chunk (ramp up / down; those sums are never stored).
-template <int K, int YPT, bool GUARD, bool UNROLL, bool ZSKIP>
+template <int K, int YPT, bool GUARD, bool UNROLL, bool SKIP, int KXS>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
                                            const int (&off)[LoadRun<K>::NOFF], int ty,
                                            const Weights<K>& wt, Accum<K, YPT>& acc, int first,
-                                           int last, uint32_t zskip) {
+                                           int last, uint32_t zskip, uint32_t yskip) {
   constexpr int SH = LoadRun<K>::SH;
   constexpr int NLD = LoadRun<K>::NLD;
   constexpr int RPF = Ready<K>::RPF;
@@ -731,12 +732,14 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
     for (int m = 0; m < K; ++m) {
       if (GUARD && (m < first || m > last)) continue;
       const int dz = K - 1 - m;
-      // z planes that only pad an f32 kernel to a cube: no FMA at all (a
-      // zero weight times an Inf would inject NaN)
-      if (ZSKIP && ((zskip >> dz) & 1u)) continue;
+      // z planes / y rows that only pad an anisotropic kernel to the K^3
+      // cube: no FMA at all (a zero weight times an Inf would inject NaN,
+      // and the FMA pipe is the bound); uniform branches per (dz, dy) row
+      if (SKIP && (((zskip >> dz) | (yskip >> dy)) & 1u)) continue;
       const float* w = wt.w + (dz * K + dy) * Weights<K>::KP;
+      // x taps: the kernel's own KXS columns of the cube (a template)
 #pragma unroll
-      for (int dx = 0; dx < K; ++dx) {
+      for (int dx = (K - KXS) / 2; dx < (K + KXS) / 2; ++dx) {
         const float wv = w[dx];
 #pragma unroll
         for (int r = 0; r < YPT; ++r)
@@ -747,7 +750,7 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
   }
 }
 
-template <typename T, int K, int MODE, bool ZSKIP = false>
+template <typename T, int K, int MODE, bool SKIP = false, int KXS = K>
 __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
                                   Layout<(int)sizeof(T), K>::CTAS_PER_SM)
     filter_tma_kernel(const __grid_constant__ CUtensorMap map_src,
@@ -928,9 +931,10 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     constexpr bool UNROLL = K <= 7;  // K = 9 unrolled: ~2900 FFMA2 per plane body
     constexpr bool UNROLL_G = K <= 5;  // K = 5 with rolled ramps: 4.60 vs 4.46 ms
     if (first <= 0 && last >= K - 1)
-      plane_step<K, YPT, false, UNROLL, ZSKIP>(stage, ld_off, ty, wt, acc, 0, K - 1, p.zskip);
+      plane_step<K, YPT, false, UNROLL, SKIP, KXS>(stage, ld_off, ty, wt, acc, 0, K - 1, p.zskip, p.yskip);
     else
-      plane_step<K, YPT, true, UNROLL_G, ZSKIP>(stage, ld_off, ty, wt, acc, first, last, p.zskip);
+      plane_step<K, YPT, true, UNROLL_G, SKIP, KXS>(stage, ld_off, ty, wt, acc, first, last, p.zskip,
+                                                    p.yskip);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
@@ -957,14 +961,14 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   }
 }
 
-template <typename T, int K, int MODE, bool ZSKIP = false>
+template <typename T, int K, int MODE, bool SKIP = false, int KXS = K>
 cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, const CUtensorMap& mh,
                               const TmaParams& p, const float* w32, dim3 grid, cudaStream_t s) {
   using C = Cfg<T, K>;
   Weights<K> wt = {};
   for (int r = 0; r < K * K; ++r)
     for (int x = 0; x < K; ++x) wt.w[r * Weights<K>::KP + x] = w32[r * K + x];
-  auto fn = filter_tma_kernel<T, K, MODE, ZSKIP>;
+  auto fn = filter_tma_kernel<T, K, MODE, SKIP, KXS>;
   // the shared-memory opt-in once per device (a per-call attribute set was a
   // measurable share of the host time of small launches)
   static std::atomic<uint64_t> opted{0};

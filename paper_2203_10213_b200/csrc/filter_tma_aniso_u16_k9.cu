@@ -1,0 +1,34 @@
+// filter_tma_aniso_u16_k9.cu — anisotropic u16 kernels in a 9^3 cube: x extent
+// kxs in {1, 3, ..., 9} as a template, padding y rows / z planes skipped by
+// mask (filter_tma.cuh plane_step; vkt_capi.cu pad_to_cube).  One file per
+// (format, K) so the 4 x (K+1)/2 x 4 specialisations compile in parallel.
+#include "filter_tma.cuh"
+
+namespace vkt {
+namespace tma {
+template <typename T>
+cudaError_t launch_tma_aniso_k9(int kxs, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
+                                 const CUtensorMap& mh, const TmaParams& p, const float* w32,
+                                 dim3 grid, cudaStream_t s);
+template <>
+cudaError_t launch_tma_aniso_k9<uint16_t>(int kxs, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
+                                      const CUtensorMap& mh, const TmaParams& p, const float* w32,
+                                      dim3 grid, cudaStream_t s) {
+#define VKT_ANISO_CASE(KX, MM) \
+  if (kxs == KX && mode == MM) return launch_tma_kernel<uint16_t, 9, MM, true, KX>(ms, ml, mh, p, w32, grid, s);
+#define VKT_ANISO_KX(KX)         \
+  VKT_ANISO_CASE(KX, VKT_WRAP)   \
+  VKT_ANISO_CASE(KX, VKT_MIRROR) \
+  VKT_ANISO_CASE(KX, VKT_CLAMP)  \
+  VKT_ANISO_CASE(KX, VKT_BORDER)
+  VKT_ANISO_KX(1)
+  VKT_ANISO_KX(3)
+  VKT_ANISO_KX(5)
+  VKT_ANISO_KX(7)
+  VKT_ANISO_KX(9)
+#undef VKT_ANISO_KX
+#undef VKT_ANISO_CASE
+  return cudaErrorInvalidValue;
+}
+}  // namespace tma
+}  // namespace vkt

@@ -19,27 +19,18 @@ cudaError_t launch_tma_dtype<float>(int k, int mode, const CUtensorMap& ms, cons
     std::memcpy(&zp, &p, sizeof zp);
     return tma_zp::launch_tma_dtype<float>(k, mode, ms, ml, mh, zp, w32, grid, s);
   }
-#define VKT_F32_MODES(KK, Z)                                                                     \
-  switch (mode) {                                                                               \
-    case VKT_WRAP: return launch_tma_kernel<float, KK, VKT_WRAP, Z>(ms, ml, mh, p, w32, grid, s);     \
-    case VKT_MIRROR: return launch_tma_kernel<float, KK, VKT_MIRROR, Z>(ms, ml, mh, p, w32, grid, s); \
-    case VKT_CLAMP: return launch_tma_kernel<float, KK, VKT_CLAMP, Z>(ms, ml, mh, p, w32, grid, s);   \
-    case VKT_BORDER: return launch_tma_kernel<float, KK, VKT_BORDER, Z>(ms, ml, mh, p, w32, grid, s); \
-    default: return cudaErrorInvalidValue;                                                      \
-  }
-  // p.zskip != 0: an anisotropic f32 kernel padded in z to a cube (vkt_capi.cu)
-#define VKT_F32_CASES(KK)        \
-  if (k == KK) {                 \
-    if (p.zskip != 0)            \
-      VKT_F32_MODES(KK, true)    \
-    else                         \
-      VKT_F32_MODES(KK, false)   \
-  }
+#define VKT_F32_CASES(KK)                                                                       \
+  if (k == KK) switch (mode) {                                                                   \
+      case VKT_WRAP: return launch_tma_kernel<float, KK, VKT_WRAP>(ms, ml, mh, p, w32, grid, s);     \
+      case VKT_MIRROR: return launch_tma_kernel<float, KK, VKT_MIRROR>(ms, ml, mh, p, w32, grid, s); \
+      case VKT_CLAMP: return launch_tma_kernel<float, KK, VKT_CLAMP>(ms, ml, mh, p, w32, grid, s);   \
+      case VKT_BORDER: return launch_tma_kernel<float, KK, VKT_BORDER>(ms, ml, mh, p, w32, grid, s); \
+      default: return cudaErrorInvalidValue;                                                     \
+    }
   VKT_F32_CASES(5)
   VKT_F32_CASES(7)
   VKT_F32_CASES(9)
 #undef VKT_F32_CASES
-#undef VKT_F32_MODES
   return cudaErrorInvalidValue;
 }
 }  // namespace tma

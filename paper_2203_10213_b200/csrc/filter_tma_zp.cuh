@@ -148,6 +148,7 @@ struct TmaParams {
   int64_t z_offset, global_nz;
   float c;
   uint32_t zskip;
+  uint32_t yskip;
   const int* guard;
 };
 

@@ -150,21 +150,24 @@ static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
   return VKT_OK;
 }
 
-// Anisotropic integer kernels on the tiled kernel: embed the (kx, ky, kz)
-// weights centred in a K^3 cube of zeros, K = max extent.  Integer voxels
-// widen to finite non-negative floats, so every added tap contributes an
-// exact +0 and the FP32 sums -- the same nonzero products in the same
-// relative (dz, dy, dx) order -- are bit-identical to the unpadded ones.
-// f32 volumes padded only in z run as they are: the kernel skips the padding
-// planes outright (a zero weight times an Inf would inject NaN).  Other f32
-// kernels (x/y padding, or K = 3, whose direct-staging kernel cannot skip)
-// are `guarded`: an Inf/NaN scan of the source and its halo planes picks, on
-// the device, the tiled launch when every voxel is finite (each added tap is
-// then an exact +0 again) or the direct kernel otherwise.
+// Anisotropic kernels on the tiled kernels: embed the (kx, ky, kz) weights,
+// centred, in a K^3 cube of zeros, K = max extent.
+//  * K >= 5 (the paired-layout kernel): the kernel runs only the real taps:
+//    its x extent kx is a template and the padding y rows / z planes are
+//    skipped by mask (yskip / zskip).  So no FMA is wasted and no zero weight
+//    ever meets an Inf (results bit-identical to the direct kernel's, Inf and
+//    NaN voxels included).
+//  * K = 3, integer voxels (the warp kernel): the cube is evaluated densely;
+//    integer voxels widen to finite floats, so each added tap is an exact +0
+//    and the FP32 sums -- the same nonzero products in the same relative
+//    (dz, dy, dx) order -- are bit-identical to the unpadded ones.
+//  * K = 3, f32 (the direct-staging kernel, which cannot skip): `guarded` --
+//    an Inf/NaN scan of the source and its halo planes picks, on the device,
+//    the tiled launch when every voxel is finite or the direct kernel.
 // The z extent may only grow when no halo buffers are involved: halos are
 // sized for the caller's kz.
 static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vector<double>& w,
-                        uint32_t& zskip, bool& guarded) {
+                        FilterPlan& skip, bool& guarded) {
   if (a->flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
   const int kx = a->kdims.x, ky = a->kdims.y, kz = a->kdims.z;
   if (kx == ky && ky == kz) return false;
@@ -173,7 +176,7 @@ static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vec
   if (k != 3 && k != 5 && k != 7 && k != 9) return false;
   const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
                          (a->global_nz <= 0 || a->global_nz == a->dims.z);
-  guarded = a->format == VKT_F32 && (kx != k || ky != k || k == 3);
+  guarded = a->format == VKT_F32 && k == 3;
   if (kz != k && !unsharded) return false;
   w.assign((size_t)k * k * k, 0.0);
   const int ox = (k - kx) / 2, oy = (k - ky) / 2, oz = (k - kz) / 2;
@@ -184,10 +187,15 @@ static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vec
   out = *a;
   out.kdims = vkt_int3{k, k, k};
   out.weights = w.data();
-  zskip = 0;
-  if (a->format == VKT_F32 && k != 3)
-    for (int z = 0; z < k; ++z)
-      if (z < oz || z >= oz + kz) zskip |= 1u << z;
+  skip.kxs = 0;
+  skip.zskip = skip.yskip = 0;
+  if (k >= 5) {
+    skip.kxs = kx;
+    for (int i = 0; i < k; ++i) {
+      if (i < oz || i >= oz + kz) skip.zskip |= 1u << i;
+      if (i < oy || i >= oy + ky) skip.yskip |= 1u << i;
+    }
+  }
   return true;
 }
 
@@ -242,12 +250,14 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;
-    uint32_t zskip = 0;
+    FilterPlan skip;
     bool guarded = false;
-    if (pad_to_cube(args, cube, wcube, zskip, guarded)) {
+    if (pad_to_cube(args, cube, wcube, skip, guarded)) {
       FilterPlan p2;
       if (validate_and_plan(&cube, p2) == VKT_OK && p2.path == VKT_PATH_TMA) {
-        p2.zskip = zskip;
+        p2.kxs = skip.kxs;
+        p2.zskip = skip.zskip;
+        p2.yskip = skip.yskip;
         if (p2.z_end <= p2.z_begin) return VKT_OK;
         cudaStream_t s2 = reinterpret_cast<cudaStream_t>(stream);
         const int st2 = guarded ? launch_guarded(plan, p2, s2) : launch_filter_tma(p2, s2);
@@ -271,10 +281,9 @@ int vkt_filter_path(const vkt_filter_args* args) {
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;
-    FilterPlan p2;
-    uint32_t zskip = 0;
+    FilterPlan p2, skip;
     bool guarded = false;
-    if (pad_to_cube(args, cube, wcube, zskip, guarded) && validate_and_plan(&cube, p2) == VKT_OK)
+    if (pad_to_cube(args, cube, wcube, skip, guarded) && validate_and_plan(&cube, p2) == VKT_OK)
       return p2.path;
   }
   return plan.path;
@@ -286,10 +295,9 @@ int vkt_filter_chunk_planes(const vkt_filter_args* args) {
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;
-    FilterPlan p2;
-    uint32_t zskip = 0;
+    FilterPlan p2, skip;
     bool guarded = false;
-    if (pad_to_cube(args, cube, wcube, zskip, guarded) && validate_and_plan(&cube, p2) == VKT_OK &&
+    if (pad_to_cube(args, cube, wcube, skip, guarded) && validate_and_plan(&cube, p2) == VKT_OK &&
         p2.path == VKT_PATH_TMA)
       return tma_chunk_planes(p2);
     return 0;

@@ -158,14 +158,16 @@ def test_anisotropic_f32_z_padded_on_the_tiled_path(kd):
     assert ok, (kd, ndiff, dmax)
 
 
-@pytest.mark.parametrize("kd", [(3, 1, 5), (5, 3, 5), (3, 3, 1), (1, 3, 3), (7, 5, 3), (9, 1, 1)],
+@pytest.mark.parametrize("kd", [(3, 1, 5), (5, 3, 5), (3, 3, 1), (1, 3, 3), (7, 5, 3), (9, 1, 1),
+                                (1, 1, 9), (1, 7, 1)],
                          ids=lambda k: "x".join(map(str, k)))
 @pytest.mark.parametrize("nx", [140, 141])
-def test_anisotropic_f32_guarded_cube(kd, nx):
-    """Other anisotropic f32 kernels (x/y padding, or K = 3) run cube-padded
-    behind an on-device Inf/NaN scan: finite volumes take the tiled kernel,
-    whose added zero taps are exact +0, and match the direct kernel; a volume
-    holding Inf or NaN takes the direct kernel and matches it bitwise."""
+def test_anisotropic_f32_cube(kd, nx):
+    """Anisotropic f32 kernels on the tiled kernels.  K >= 5 cubes run only
+    the real taps (x extent templated, padding rows / planes skipped), so they
+    match the direct kernel bitwise on any volume, Inf / NaN included; K = 3
+    cubes run behind an on-device Inf/NaN scan (finite: tiled, exact +0 zero
+    taps; otherwise the direct kernel)."""
     rng = np.random.default_rng(11 + sum(kd) + nx)
     finite = rng.random((9, 23, nx), dtype=np.float32) - np.float32(0.25)
     w = rng.random(kd[::-1]) - 0.2

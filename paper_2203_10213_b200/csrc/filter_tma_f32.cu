@@ -1,9 +1,7 @@
 // filter_tma_f32.cu — the tiled TMA kernels for float voxels (K in {3,5,7,9} x
-// the four address modes): K = 5, 7 on the paired-layout kernel
+// the four address modes): K = 5, 7, 9 on the paired-layout kernel
 // (filter_tma.cuh), K = 3 on the direct-staging variant (filter_tma_zp.cuh,
 // see its header).
-#include <cstring>
-
 #include "filter_tma.cuh"
 #include "filter_tma_zp.cuh"
 
@@ -13,12 +11,7 @@ template <>
 cudaError_t launch_tma_dtype<float>(int k, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
                                     const CUtensorMap& mh, const TmaParams& p, const float* w32,
                                     dim3 grid, cudaStream_t s) {
-  if (k == 3) {
-    static_assert(sizeof(tma_zp::TmaParams) == sizeof(TmaParams), "parameter layouts");
-    tma_zp::TmaParams zp;
-    std::memcpy(&zp, &p, sizeof zp);
-    return tma_zp::launch_tma_dtype<float>(k, mode, ms, ml, mh, zp, w32, grid, s);
-  }
+  if (k == 3) return tma_zp::launch_f32_k3(mode, ms, ml, mh, p, w32, grid, s);
 #define VKT_F32_CASES(KK)                                                                       \
   if (k == KK) switch (mode) {                                                                   \
       case VKT_WRAP: return launch_tma_kernel<float, KK, VKT_WRAP>(ms, ml, mh, p, w32, grid, s);     \

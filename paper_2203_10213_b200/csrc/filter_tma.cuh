@@ -260,6 +260,13 @@ __device__ __forceinline__ void ffma2_bw(uint64_t x, float w, uint64_t& c) {
   // rolled dy loop instead of being renamed with moves at the back edge
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(x), "l"(f2pack(w, w)));
 }
+// x * w + c0 into another accumulator (an untied destination: starts a slot
+// from the next slot's partial sum or the epilogue constant without a copy).
+__device__ __forceinline__ uint64_t ffma2_from(uint64_t x, float w, uint64_t c0) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(f2pack(w, w)), "l"(c0));
+  return d;
+}
 // Two u8/u16 values, given as the bit patterns 0x4B000000 | v (the value in
 // the low mantissa bits of 2^23), -> (float, float) exactly: minus 2^23, one
 // FADD2.
@@ -706,11 +713,18 @@ struct LoadRun {
 // One input plane's contribution to the K rolling accumulators of the
 // thread's YPT x 4 output pairs.  GUARD: skip slots whose output plane is
 // outside the chunk (ramp up / down; those sums are never stored).
-template <int K, int YPT, bool GUARD, bool UNROLL, bool SKIP, int KXS>
+// ROLL_IN (steady planes of the unrolled, unskipped kernels): the plane's
+// first tap into slot m (dy = dx = 0) reads slot m+1 -- the partial sum one
+// output plane later -- or the epilogue constant a00 for slot K-1, and writes
+// slot m, so the accumulators roll without register moves.  Other planes
+// roll explicitly before their taps (roll_slots).
+template <int K, int YPT, bool GUARD, bool UNROLL, bool SKIP, int KXS, bool ROLL_IN = false>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
                                            const int (&off)[LoadRun<K>::NOFF], int ty,
                                            const Weights<K>& wt, Accum<K, YPT>& acc, int first,
-                                           int last, uint32_t zskip, uint32_t yskip) {
+                                           int last, uint32_t zskip, uint32_t yskip,
+                                           uint64_t a00 = 0) {
+  static_assert(!ROLL_IN || (UNROLL && !GUARD && !SKIP), "in-FMA roll needs every tap, unrolled");
   constexpr int SH = LoadRun<K>::SH;
   constexpr int NLD = LoadRun<K>::NLD;
   constexpr int RPF = Ready<K>::RPF;
@@ -747,7 +761,12 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
 #pragma unroll
         for (int r = 0; r < YPT; ++r)
 #pragma unroll
-          for (int j = 0; j < XQ; ++j) ffma2_bw(P[r][j + dx + SH], wv, acc.p[r][m][j]);
+          for (int j = 0; j < XQ; ++j) {
+            if (ROLL_IN && dy == 0 && dx == 0)
+              acc.p[r][m][j] = ffma2_from(P[r][j + dx + SH], wv, m + 1 < K ? acc.p[r][m + 1 < K ? m + 1 : m][j] : a00);
+            else
+              ffma2_bw(P[r][j + dx + SH], wv, acc.p[r][m][j]);
+          }
       }
     }
   }
@@ -933,11 +952,30 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     // -> 11.11 ms for f32, against all-rolled / all-unrolled).
     constexpr bool UNROLL = K <= 7;  // K = 9 unrolled: ~2900 FFMA2 per plane body
     constexpr bool UNROLL_G = K <= 5;  // K = 5 with rolled ramps: 4.60 vs 4.46 ms
-    if (first <= 0 && last >= K - 1)
-      plane_step<K, YPT, false, UNROLL, SKIP, KXS>(stage, ld_off, ty, wt, acc, 0, K - 1, p.zskip, p.yskip);
-    else
+    // accumulators after plane i-1 still hold slot m = output plane
+    // zo0 + i-1 - 2R + m; the plane's first taps (ROLL_IN) or roll_slots
+    // shift them by one (the former IMAD.MOV roll after every plane: ~3.5%
+    // of the K = 7 instructions)
+    constexpr bool ROLL_IN = UNROLL && !SKIP;
+    auto roll_slots = [&]() {
+#pragma unroll
+      for (int r = 0; r < YPT; ++r)
+#pragma unroll
+        for (int j = 0; j < XQ; ++j) {
+#pragma unroll
+          for (int m = 0; m + 1 < K; ++m) acc.p[r][m][j] = acc.p[r][m + 1][j];
+          acc.p[r][K - 1][j] = a00;
+        }
+    };
+    if (first <= 0 && last >= K - 1) {
+      if constexpr (!ROLL_IN) roll_slots();
+      plane_step<K, YPT, false, UNROLL, SKIP, KXS, ROLL_IN>(stage, ld_off, ty, wt, acc, 0, K - 1, p.zskip,
+                                                            p.yskip, a00);
+    } else {
+      roll_slots();
       plane_step<K, YPT, true, UNROLL_G, SKIP, KXS>(stage, ld_off, ty, wt, acc, first, last, p.zskip,
                                                     p.yskip);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
@@ -952,15 +990,6 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
         if (st_hi) store4<T>(o + HALF, f2hi(a[0]), f2hi(a[1]), f2hi(a[2]), f2hi(a[3]));
       }
     }
-    // roll: slot m <- slot m+1, slot K-1 <- fresh
-#pragma unroll
-    for (int r = 0; r < YPT; ++r)
-#pragma unroll
-      for (int j = 0; j < XQ; ++j) {
-#pragma unroll
-        for (int m = 0; m + 1 < K; ++m) acc.p[r][m][j] = acc.p[r][m + 1][j];
-        acc.p[r][K - 1][j] = a00;
-      }
   }
 }
 

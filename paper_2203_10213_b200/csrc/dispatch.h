@@ -24,6 +24,7 @@ struct FilterPlan {
   int kxs = 0;
   uint32_t zskip = 0;       // bit dz set: padding plane
   uint32_t yskip = 0;       // bit dy set: padding row
+  bool zthin = false;       // kz = 1: the kernel variant with one z slot (no halo, no roll)
   // Device flag set by launch_scan_nonfinite.  Tiled launches do nothing when
   // it is set, direct launches only then; nullptr = unconditional.
   const int* guard = nullptr;

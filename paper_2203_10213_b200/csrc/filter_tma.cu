@@ -33,12 +33,12 @@ cudaError_t launch_tma_dtype<float>(int, int, const CUtensorMap&, const CUtensor
                                     cudaStream_t);
 #define VKT_ANISO_DECL(KK, T)                                                                      \
   template <>                                                                                     \
-  cudaError_t launch_tma_aniso_k##KK<T>(int, int, const CUtensorMap&, const CUtensorMap&,        \
+  cudaError_t launch_tma_aniso_k##KK<T>(int, bool, int, const CUtensorMap&, const CUtensorMap&,  \
                                         const CUtensorMap&, const TmaParams&, const float*, dim3, \
                                         cudaStream_t);
 #define VKT_ANISO_DECLS(KK)                                                                     \
   template <typename T>                                                                         \
-  cudaError_t launch_tma_aniso_k##KK(int, int, const CUtensorMap&, const CUtensorMap&,         \
+  cudaError_t launch_tma_aniso_k##KK(int, bool, int, const CUtensorMap&, const CUtensorMap&,   \
                                      const CUtensorMap&, const TmaParams&, const float*, dim3,  \
                                      cudaStream_t);                                              \
   VKT_ANISO_DECL(KK, uint8_t)                                                                   \
@@ -53,13 +53,13 @@ VKT_ANISO_DECLS(9)
 // Anisotropic kernels embedded in a K^3 cube: x extent kxs <= K a template,
 // padding y rows / z planes skipped by mask (filter_tma_aniso_<fmt>_k<K>.cu).
 template <typename T>
-cudaError_t launch_tma_aniso(int k, int kxs, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
-                             const CUtensorMap& mh, const TmaParams& p, const float* w32, dim3 grid,
-                             cudaStream_t s) {
+cudaError_t launch_tma_aniso(int k, int kxs, bool zthin, int mode, const CUtensorMap& ms,
+                             const CUtensorMap& ml, const CUtensorMap& mh, const TmaParams& p,
+                             const float* w32, dim3 grid, cudaStream_t s) {
   switch (k) {
-    case 5: return launch_tma_aniso_k5<T>(kxs, mode, ms, ml, mh, p, w32, grid, s);
-    case 7: return launch_tma_aniso_k7<T>(kxs, mode, ms, ml, mh, p, w32, grid, s);
-    case 9: return launch_tma_aniso_k9<T>(kxs, mode, ms, ml, mh, p, w32, grid, s);
+    case 5: return launch_tma_aniso_k5<T>(kxs, zthin, mode, ms, ml, mh, p, w32, grid, s);
+    case 7: return launch_tma_aniso_k7<T>(kxs, zthin, mode, ms, ml, mh, p, w32, grid, s);
+    case 9: return launch_tma_aniso_k9<T>(kxs, zthin, mode, ms, ml, mh, p, w32, grid, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -238,16 +238,16 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   switch (a.format) {
     case VKT_U8:
       err = wk      ? tmaw::launch_warp_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
-            : aniso ? tma::launch_tma_aniso<uint8_t>(k, plan.kxs, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+            : aniso ? tma::launch_tma_aniso<uint8_t>(k, plan.kxs, plan.zthin, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
                     : tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     case VKT_U16:
       err = wk      ? tmaw::launch_warp_dtype<uint16_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
-            : aniso ? tma::launch_tma_aniso<uint16_t>(k, plan.kxs, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+            : aniso ? tma::launch_tma_aniso<uint16_t>(k, plan.kxs, plan.zthin, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
                     : tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     default:
-      err = aniso ? tma::launch_tma_aniso<float>(k, plan.kxs, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+      err = aniso ? tma::launch_tma_aniso<float>(k, plan.kxs, plan.zthin, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
                   : tma::launch_tma_dtype<float>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
   }

@@ -718,10 +718,11 @@ struct LoadRun {
 // output plane later -- or the epilogue constant a00 for slot K-1, and writes
 // slot m, so the accumulators roll without register moves.  Other planes
 // roll explicitly before their taps (roll_slots).
-template <int K, int YPT, bool GUARD, bool UNROLL, bool SKIP, int KXS, bool ROLL_IN = false>
+template <int K, int YPT, bool GUARD, bool UNROLL, bool SKIP, int KXS, bool ROLL_IN = false,
+          int KZS = K>
 __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
                                            const int (&off)[LoadRun<K>::NOFF], int ty,
-                                           const Weights<K>& wt, Accum<K, YPT>& acc, int first,
+                                           const Weights<K>& wt, Accum<KZS, YPT>& acc, int first,
                                            int last, uint32_t zskip, uint32_t yskip,
                                            uint64_t a00 = 0) {
   static_assert(!ROLL_IN || (UNROLL && !GUARD && !SKIP), "in-FMA roll needs every tap, unrolled");
@@ -746,9 +747,11 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
       }
     }
 #pragma unroll
-    for (int m = 0; m < K; ++m) {
+    for (int m = 0; m < KZS; ++m) {
       if (GUARD && (m < first || m > last)) continue;
-      const int dz = K - 1 - m;
+      // slot m of the KZS z slots; a z-thin variant (KZS = 1) has only the
+      // cube's centre plane
+      const int dz = (K - KZS) / 2 + KZS - 1 - m;
       // z planes / y rows that only pad an anisotropic kernel to the K^3
       // cube: no FMA at all (a zero weight times an Inf would inject NaN,
       // and the FMA pipe is the bound); uniform branches per (dz, dy) row
@@ -763,7 +766,7 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
 #pragma unroll
           for (int j = 0; j < XQ; ++j) {
             if (ROLL_IN && dy == 0 && dx == 0)
-              acc.p[r][m][j] = ffma2_from(P[r][j + dx + SH], wv, m + 1 < K ? acc.p[r][m + 1 < K ? m + 1 : m][j] : a00);
+              acc.p[r][m][j] = ffma2_from(P[r][j + dx + SH], wv, m + 1 < KZS ? acc.p[r][m + 1 < KZS ? m + 1 : m][j] : a00);
             else
               ffma2_bw(P[r][j + dx + SH], wv, acc.p[r][m][j]);
           }
@@ -772,7 +775,7 @@ __device__ __forceinline__ void plane_step(const float* __restrict__ stage,
   }
 }
 
-template <typename T, int K, int MODE, bool SKIP = false, int KXS = K>
+template <typename T, int K, int MODE, bool SKIP = false, int KXS = K, int KZS = K>
 __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
                                   Layout<(int)sizeof(T), K>::CTAS_PER_SM)
     filter_tma_kernel(const __grid_constant__ CUtensorMap map_src,
@@ -820,7 +823,9 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   const int zo0 = p.z_begin + blockIdx.z * p.zc;
   const int nzo = min(p.zc, p.z_end - zo0);
   if (nzo <= 0) return;
-  const int np = nzo + 2 * R;  // input planes of this chunk
+  // KZS z slots: K, or 1 for a z-thin anisotropic kernel (no z halo, no roll)
+  constexpr int RZ = KZS / 2;
+  const int np = nzo + 2 * RZ;  // input planes of this chunk
   const bool edge = (x0 - R < 0) || (x0 + TX + R > p.nx) || (y0 - R < 0) || (y0 + TY + R > p.ny);
 
   if (tid == 0) {
@@ -847,7 +852,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   const bool leader = tid == 0;
   auto issue = [&](int j) {
     const int r = j % SR;
-    const PlaneSrc s = resolve<MODE>(p, R, zo0 - R + j);
+    const PlaneSrc s = resolve<MODE>(p, RZ, zo0 - RZ + j);
     if (s.which < 0) {
       mbar_arrive_if(&full[r], leader);
       return;
@@ -863,7 +868,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   constexpr int WSTEP = SPLIT ? 2 : 1;  // the next plane this warp half stages
   WrapList<T, K, ST> wlist(p, x0, y0, WLIST && edge, tid % ST);
   if (WLIST && edge && (SPLIT ? half : 0) < np)
-    wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + (SPLIT ? half : 0))));
+    wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, RZ, zo0 - RZ + (SPLIT ? half : 0))));
   auto prepare = [&](int j) {
     if (SPLIT && half != (j & 1)) return;
     VKT_JITTER_POINT(4 * j);
@@ -872,7 +877,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     const int r = j % SR;
     mbar_wait(&full[r], (uint32_t)((j / SR) & 1));
     if (j >= S) mbar_wait(&empty[s], (uint32_t)(((j / S) - 1) & 1));
-    const PlaneSrc src = resolve<MODE>(p, R, zo0 - R + j);
+    const PlaneSrc src = resolve<MODE>(p, RZ, zo0 - RZ + j);
     if (src.which < 0) {
       float4* w4 = reinterpret_cast<float4*>(stage);
       for (int q = tid % ST; q < C::RDY_BYTES / 16; q += ST) w4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -885,7 +890,7 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
           // after the whole half's main pass (it wrote the zero fill there)
           asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(ST) : "memory");
           wlist.apply(stage, plane_ptr<T>(p, src), p, x0, y0, tid % ST);
-          if (j + WSTEP < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, R, zo0 - R + j + WSTEP)));
+          if (j + WSTEP < np) wlist.gather(plane_ptr<T>(p, resolve<MODE>(p, RZ, zo0 - RZ + j + WSTEP)));
         }
       }
     }
@@ -907,11 +912,11 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   LoadRun<K>::offsets(tx, ld_off);
   const float a0 = acc_init<T>(p.c);
   const uint64_t a00 = f2pack(a0, a0);
-  Accum<K, YPT> acc;
+  Accum<KZS, YPT> acc;
 #pragma unroll
   for (int r = 0; r < YPT; ++r)
 #pragma unroll
-    for (int m = 0; m < K; ++m)
+    for (int m = 0; m < KZS; ++m)
 #pragma unroll
       for (int j = 0; j < XQ; ++j) acc.p[r][m][j] = a00;
 
@@ -944,8 +949,8 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
     if (i + C::AHEAD < np) prepare(i + C::AHEAD);
     mbar_wait(&ready[s], (uint32_t)((i / S) & 1));
     // slot m <-> output plane zo0 + i - 2R + m
-    const int first = 2 * R - i;
-    const int last = nzo - 1 - i + 2 * R;
+    const int first = 2 * RZ - i;
+    const int last = nzo - 1 - i + 2 * RZ;
     // The steady-state planes run the dy loop unrolled; the ramp planes
     // (GUARD, 2R of every chunk's ~70) keep it rolled at K = 7, which keeps
     // the kernel's hot code compact (K = 7: 11.76 -> 11.33 ms for u16, 11.39
@@ -963,24 +968,24 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
 #pragma unroll
         for (int j = 0; j < XQ; ++j) {
 #pragma unroll
-          for (int m = 0; m + 1 < K; ++m) acc.p[r][m][j] = acc.p[r][m + 1][j];
-          acc.p[r][K - 1][j] = a00;
+          for (int m = 0; m + 1 < KZS; ++m) acc.p[r][m][j] = acc.p[r][m + 1][j];
+          acc.p[r][KZS - 1][j] = a00;
         }
     };
-    if (first <= 0 && last >= K - 1) {
+    if (first <= 0 && last >= KZS - 1) {
       if constexpr (!ROLL_IN) roll_slots();
-      plane_step<K, YPT, false, UNROLL, SKIP, KXS, ROLL_IN>(stage, ld_off, ty, wt, acc, 0, K - 1, p.zskip,
-                                                            p.yskip, a00);
+      plane_step<K, YPT, false, UNROLL, SKIP, KXS, ROLL_IN, KZS>(stage, ld_off, ty, wt, acc, 0, KZS - 1,
+                                                                 p.zskip, p.yskip, a00);
     } else {
       roll_slots();
-      plane_step<K, YPT, true, UNROLL_G, SKIP, KXS>(stage, ld_off, ty, wt, acc, first, last, p.zskip,
-                                                    p.yskip);
+      plane_step<K, YPT, true, UNROLL_G, SKIP, KXS, false, KZS>(stage, ld_off, ty, wt, acc, first, last,
+                                                                p.zskip, p.yskip);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
 
-    if (i >= 2 * R) {
-      const int oz = zo0 + i - 2 * R;
+    if (i >= 2 * RZ) {
+      const int oz = zo0 + i - 2 * RZ;
 #pragma unroll
       for (int r = 0; r < YPT; ++r) {
         if (!row_ok[r]) continue;
@@ -993,14 +998,14 @@ __global__ void __launch_bounds__(Layout<(int)sizeof(T), K>::THREADS,
   }
 }
 
-template <typename T, int K, int MODE, bool SKIP = false, int KXS = K>
+template <typename T, int K, int MODE, bool SKIP = false, int KXS = K, int KZS = K>
 cudaError_t launch_tma_kernel(const CUtensorMap& ms, const CUtensorMap& ml, const CUtensorMap& mh,
                               const TmaParams& p, const float* w32, dim3 grid, cudaStream_t s) {
   using C = Cfg<T, K>;
   Weights<K> wt = {};
   for (int r = 0; r < K * K; ++r)
     for (int x = 0; x < K; ++x) wt.w[r * Weights<K>::KP + x] = w32[r * K + x];
-  auto fn = filter_tma_kernel<T, K, MODE, SKIP, KXS>;
+  auto fn = filter_tma_kernel<T, K, MODE, SKIP, KXS, KZS>;
   // the shared-memory opt-in once per device (a per-call attribute set was a
   // measurable share of the host time of small launches)
   static std::atomic<uint64_t> opted{0};

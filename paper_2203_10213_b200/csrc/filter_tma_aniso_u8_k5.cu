@@ -1,21 +1,24 @@
 // filter_tma_aniso_u8_k5.cu — anisotropic u8 kernels in a 5^3 cube: x extent
 // kxs in {1, 3, ..., 5} as a template, padding y rows / z planes skipped by
-// mask (filter_tma.cuh plane_step; vkt_capi.cu pad_to_cube).  One file per
+// mask (filter_tma.cuh plane_step; vkt_capi.cu pad_to_cube); z-thin kernels
+// (kz = 1) also as a variant with one z slot (no z halo, no accumulator roll).  One file per
 // (format, K) so the 4 x (K+1)/2 x 4 specialisations compile in parallel.
 #include "filter_tma.cuh"
 
 namespace vkt {
 namespace tma {
 template <typename T>
-cudaError_t launch_tma_aniso_k5(int kxs, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
+cudaError_t launch_tma_aniso_k5(int kxs, bool zthin, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
                                  const CUtensorMap& mh, const TmaParams& p, const float* w32,
                                  dim3 grid, cudaStream_t s);
 template <>
-cudaError_t launch_tma_aniso_k5<uint8_t>(int kxs, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
+cudaError_t launch_tma_aniso_k5<uint8_t>(int kxs, bool zthin, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
                                       const CUtensorMap& mh, const TmaParams& p, const float* w32,
                                       dim3 grid, cudaStream_t s) {
-#define VKT_ANISO_CASE(KX, MM) \
-  if (kxs == KX && mode == MM) return launch_tma_kernel<uint8_t, 5, MM, true, KX>(ms, ml, mh, p, w32, grid, s);
+#define VKT_ANISO_CASE(KX, MM)                                                                  \
+  if (kxs == KX && mode == MM)                                                                  \
+    return zthin ? launch_tma_kernel<uint8_t, 5, MM, true, KX, 1>(ms, ml, mh, p, w32, grid, s)      \
+                 : launch_tma_kernel<uint8_t, 5, MM, true, KX>(ms, ml, mh, p, w32, grid, s);
 #define VKT_ANISO_KX(KX)         \
   VKT_ANISO_CASE(KX, VKT_WRAP)   \
   VKT_ANISO_CASE(KX, VKT_MIRROR) \

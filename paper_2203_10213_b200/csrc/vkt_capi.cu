@@ -154,7 +154,8 @@ static int validate_and_plan(const vkt_filter_args* a, FilterPlan& plan) {
 // centred, in a K^3 cube of zeros, K = max extent.
 //  * K >= 5 (the paired-layout kernel): the kernel runs only the real taps:
 //    its x extent kx is a template and the padding y rows / z planes are
-//    skipped by mask (yskip / zskip).  So no FMA is wasted and no zero weight
+//    skipped by mask (yskip / zskip); a z-thin kernel (kz = 1) runs the
+//    variant with a single z slot (no z halo planes, no accumulator roll).  So no FMA is wasted and no zero weight
 //    ever meets an Inf (results bit-identical to the direct kernel's, Inf and
 //    NaN voxels included).
 //  * K = 3, integer voxels (the warp kernel): the cube is evaluated densely;
@@ -189,8 +190,10 @@ static bool pad_to_cube(const vkt_filter_args* a, vkt_filter_args& out, std::vec
   out.weights = w.data();
   skip.kxs = 0;
   skip.zskip = skip.yskip = 0;
+  skip.zthin = false;
   if (k >= 5) {
     skip.kxs = kx;
+    skip.zthin = kz == 1;
     for (int i = 0; i < k; ++i) {
       if (i < oz || i >= oz + kz) skip.zskip |= 1u << i;
       if (i < oy || i >= oy + ky) skip.yskip |= 1u << i;
@@ -256,6 +259,7 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
       FilterPlan p2;
       if (validate_and_plan(&cube, p2) == VKT_OK && p2.path == VKT_PATH_TMA) {
         p2.kxs = skip.kxs;
+        p2.zthin = skip.zthin;
         p2.zskip = skip.zskip;
         p2.yskip = skip.yskip;
         if (p2.z_end <= p2.z_begin) return VKT_OK;

@@ -397,6 +397,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    barrier()  # every rank's communicator is up before the first P2P batch
     for _ in range(args.warmup):
         apply_filter_sharded(dst, src, kernel, mode, group=group, exchange=exchange)
     barrier()
@@ -527,6 +528,28 @@ def run_ours(args):
                           "ms": round(kms, 4), "gvox_s": round(kv / kms / 1e6, 2),
                           "path": kpath, "roofline": r})
 
+    # At N > 1, rank 0 also times the unsharded launch over the whole volume
+    # (it fits one B200: 2 x 2.1 GB for cfg3, 2 x 34 GB for cfg4) so the line
+    # carries the parallel efficiency T1 / (N * T_N) next to the per-rank
+    # phases.  (The driver computes its own from the N = 1 run.)
+    t1 = None
+    if world > 1 and rank == 0 and not args.test_single_gpu and not args.no_t1:
+        whole = vk.synthetic_device((nx, ny, nz), fmt, seed=7, device=dev)
+        out1 = vk.StructuredVolume(whole.dims, fmt, data=vk.DeviceBuffer(whole.nbytes, device=dev, zero=False))
+        for _ in range(2):
+            vk.ApplyFilter(out1, whole, kernel, mode)
+        ts = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            vk.ApplyFilter(out1, whole, kernel, mode)
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t1 = min(ts)
+        del whole, out1
+        torch.cuda.empty_cache()
+
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
         cv, info = cpu_reference(args.config, args.cpu_budget, 1, 0)
@@ -555,6 +578,9 @@ def run_ours(args):
                 {"rank": r, "step": round(v[0], 4), "interior_kernel": round(v[1], 4),
                  "halo_exchange": round(v[2], 4), "boundary_kernels": round(v[3], 4)}
                 for r, v in enumerate(per_rank)]
+            if t1 is not None:
+                line["t1_ms"] = round(t1, 4)
+                line["efficiency_vs_1gpu"] = round(t1 / (world * ms_step), 4)
             line["overlap_note"] = ("halo exchange and boundary launches run on a comm stream "
                                     "beside the interior launch; step ~ max(interior, exchange + boundary)")
         print(json.dumps(line), flush=True)
@@ -575,6 +601,7 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-t1", action="store_true", help="N > 1: skip the unsharded 1-GPU reference launch")
     ap.add_argument("--test-single-gpu", action="store_true",
                     help="testing only: all ranks on cuda:0 over gloo (numbers are not a benchmark)")
     args = ap.parse_args()

@@ -11,7 +11,7 @@
 
 #include "dispatch.h"
 #include "filter_tma.cuh"
-#include "filter_warp.cuh"
+#include "filter_ws.cuh"
 
 namespace vkt {
 namespace tma {
@@ -64,23 +64,25 @@ cudaError_t launch_tma_aniso(int k, int kxs, bool zthin, int mode, const CUtenso
   }
 }
 }  // namespace tma
-namespace tmaw {
-extern template cudaError_t launch_warp_dtype<uint8_t>(int, const CUtensorMap&, const CUtensorMap&,
-                                                       const CUtensorMap&, const tma::TmaParams&,
-                                                       const float*, dim3, cudaStream_t);
-extern template cudaError_t launch_warp_dtype<uint16_t>(int, const CUtensorMap&, const CUtensorMap&,
-                                                        const CUtensorMap&, const tma::TmaParams&,
-                                                        const float*, dim3, cudaStream_t);
-}  // namespace tmaw
+namespace tmaws {
+extern template cudaError_t launch_ws_dtype<uint8_t>(int, const CUtensorMap&, const CUtensorMap&,
+                                                     const CUtensorMap&, const tma::TmaParams&,
+                                                     const float*, dim3, cudaStream_t);
+extern template cudaError_t launch_ws_dtype<uint16_t>(int, const CUtensorMap&, const CUtensorMap&,
+                                                      const CUtensorMap&, const tma::TmaParams&,
+                                                      const float*, dim3, cudaStream_t);
+}  // namespace tmaws
 
 namespace {
 
-// u8/u16 3x3x3 run the warp-private-staging kernel (filter_warp.cuh), with
-// 32-row tiles; everything else the paired-layout kernel's 16-row tiles.
+
+
+// u8/u16 3x3x3 run the warp-specialized kernel (filter_ws.cuh), with 32-row
+// tiles; everything else the paired-layout kernel's 16-row tiles.
 bool warp_kernel(const vkt_filter_args& a) {
   return a.format != VKT_F32 && a.kdims.x == 3;
 }
-int tile_rows(const vkt_filter_args& a) { return warp_kernel(a) ? tmaw::TY : tma::TY; }
+int tile_rows(const vkt_filter_args& a) { return warp_kernel(a) ? tmaws::TY : tma::TY; }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -140,7 +142,7 @@ int tma_chunk_planes(const FilterPlan& plan) {
   const int64_t slots = (int64_t)sm_count() * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
                                  : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
-                                 : warp_kernel(a) ? tmaw::CTAS_PER_SM
+                                 : warp_kernel(a) ? tmaws::CTAS_PER_SM
                                                   : tma::Layout<2, 3>::CTAS_PER_SM);
   // Under 3 waves the grid balances poorly: 512^3 u16 3^3 runs 0.266 ms at
   // 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves); f32 3^3 0.241 vs
@@ -237,12 +239,12 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   cudaError_t err;
   switch (a.format) {
     case VKT_U8:
-      err = wk      ? tmaw::launch_warp_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+      err = wk      ? tmaws::launch_ws_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
             : aniso ? tma::launch_tma_aniso<uint8_t>(k, plan.kxs, plan.zthin, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
                     : tma::launch_tma_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;
     case VKT_U16:
-      err = wk      ? tmaw::launch_warp_dtype<uint16_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
+      err = wk      ? tmaws::launch_ws_dtype<uint16_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
             : aniso ? tma::launch_tma_aniso<uint16_t>(k, plan.kxs, plan.zthin, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
                     : tma::launch_tma_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s);
       break;

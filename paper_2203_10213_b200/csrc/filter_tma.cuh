@@ -83,7 +83,7 @@ static_assert((2 * NPR + 4) / 4 % 2 == 1, "K >= 5 ready rows must be an odd numb
 // Thread layout (measured): 1 output row per thread, 8 warps
 // (staging split between the halves), 2 CTAs/SM (4 warps/SMSP, 128 regs).
 // Warps per SM stay a multiple of 4 so every SM sub-partition gets the same
-// number of FMA warps.  (u8/u16 K = 3 run filter_warp.cuh, f32 K = 3
+// number of FMA warps.  (u8/u16 K = 3 run filter_ws.cuh, f32 K = 3
 // filter_tma_zp.cuh.)
 template <int BPC, int K>
 struct Layout {

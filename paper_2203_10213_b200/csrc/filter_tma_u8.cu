@@ -1,7 +1,8 @@
 // filter_tma_u8.cu — instantiates the tiled TMA kernels for uint8_t voxels
-// (K in {3,5,7,9} x the four address modes); see filter_tma.cuh.
+// (K in {5,7,9} x the four address modes, filter_tma.cuh) and the 3x3x3
+// warp-specialized kernel (filter_ws.cuh).
 #include "filter_tma.cuh"
-#include "filter_warp.cuh"
+#include "filter_ws.cuh"
 
 namespace vkt {
 namespace tma {
@@ -9,9 +10,9 @@ template cudaError_t launch_tma_dtype<uint8_t>(int, int, const CUtensorMap&, con
                                            const CUtensorMap&, const TmaParams&, const float*,
                                            dim3, cudaStream_t);
 }  // namespace tma
-namespace tmaw {
-template cudaError_t launch_warp_dtype<uint8_t>(int, const CUtensorMap&, const CUtensorMap&,
-                                           const CUtensorMap&, const tma::TmaParams&, const float*,
-                                           dim3, cudaStream_t);
-}  // namespace tmaw
+namespace tmaws {
+template cudaError_t launch_ws_dtype<uint8_t>(int, const CUtensorMap&, const CUtensorMap&,
+                                         const CUtensorMap&, const tma::TmaParams&, const float*,
+                                         dim3, cudaStream_t);
+}  // namespace tmaws
 }  // namespace vkt

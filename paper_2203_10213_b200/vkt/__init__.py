@@ -24,7 +24,7 @@ Not on the path and not provided: hierarchical volumes, rendering, analysis
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 from .. import errors
 from ..benchmarks import run_benchmarks
@@ -39,7 +39,6 @@ from ..execution import (
     set_execution_policy,
     set_hardware_concurrency_override,
     timed,
-    with_policy,
 )
 from ..fill import fill, fill_range
 from ..filters import Kernel, apply_filter, box_kernel, gaussian_kernel
@@ -64,6 +63,12 @@ _DEFAULT = ExecutionPolicy()
 def get_execution_policy() -> _NativePolicy:
     """Policy last set on this thread, or the reference's CPU default."""
     return explicit_policy() or _DEFAULT
+
+
+def with_policy(**changes) -> _NativePolicy:
+    """Copy of the current policy with fields replaced, not installed
+    (execution.py:199-201)."""
+    return replace(get_execution_policy(), **changes)
 
 
 class StructuredVolume(_DeviceVolume):

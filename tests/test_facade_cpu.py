@@ -98,3 +98,9 @@ def test_cli_error_line_format():
 
     assert cli._error_line(vk.InvalidArgument("bad")) == "error: InvalidArgument: bad\n"
     assert cli._error_line(FileNotFoundError(2, "No such file")).startswith("error: IoFailure: ")
+
+
+def test_with_policy_uses_the_reference_default():
+    p = vkt.with_policy(worker_count=5)
+    assert p.device is vkt.Device.CPU and p.worker_count == 5
+    assert vkt.get_execution_policy().worker_count == 0  # not installed

@@ -74,11 +74,17 @@ enum {
   /* vkt_apply_filter_host only: bound device memory to a few chunks (the
    * input streams through ring buffers, halos copied device-to-device)
    * instead of keeping the padded input resident when it fits. */
-  VKT_FLAG_HOST_BOUNDED = 4
+  VKT_FLAG_HOST_BOUNDED = 4,
+  /* Never take the separable path: rank-1 kernels run the dense tiled
+   * kernels, bit-identical to the direct kernel. */
+  VKT_FLAG_NO_SEPARABLE = 8
 };
 
 /* Kernel paths reported by vkt_filter_path() */
-enum { VKT_PATH_NONE = 0, VKT_PATH_DIRECT = 1, VKT_PATH_EXACT = 2, VKT_PATH_TMA = 3 };
+/* VKT_PATH_SEPARABLE: rank-1 weights (gaussian_kernel, box_kernel) as three
+ * fused 1-D passes; within the reference contract, not bit-identical to the
+ * dense paths. */
+enum { VKT_PATH_NONE = 0, VKT_PATH_DIRECT = 1, VKT_PATH_EXACT = 2, VKT_PATH_TMA = 3, VKT_PATH_SEPARABLE = 4 };
 
 typedef struct {
   const void* src;      /* device, local slab: dims.x*dims.y*dims.z cells      */

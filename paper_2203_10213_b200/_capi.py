@@ -24,8 +24,10 @@ WRAP, MIRROR, CLAMP, BORDER = 0, 1, 2, 3
 FLAG_EXACT_F64 = 1
 FLAG_FORCE_DIRECT = 2
 FLAG_HOST_BOUNDED = 4
-PATH_NONE, PATH_DIRECT, PATH_EXACT, PATH_TMA = 0, 1, 2, 3
-PATH_NAMES = {PATH_NONE: "none", PATH_DIRECT: "direct", PATH_EXACT: "exact", PATH_TMA: "tma"}
+FLAG_NO_SEPARABLE = 8
+PATH_NONE, PATH_DIRECT, PATH_EXACT, PATH_TMA, PATH_SEPARABLE = 0, 1, 2, 3, 4
+PATH_NAMES = {PATH_NONE: "none", PATH_DIRECT: "direct", PATH_EXACT: "exact", PATH_TMA: "tma",
+              PATH_SEPARABLE: "separable"}
 
 EXPORTED_SYMBOLS = (
     "vkt_apply_filter",

@@ -28,6 +28,11 @@ struct FilterPlan {
   // Device flag set by launch_scan_nonfinite.  Tiled launches do nothing when
   // it is set, direct launches only then; nullptr = unconditional.
   const int* guard = nullptr;
+  // Separable kernels (filter_sep.cuh): the args are the K^3 cube, the
+  // weights factor as fz[dz]*fy[dy]*fx[dx] (each padded to K, centred).
+  bool sep = false;
+  std::vector<float> fx, fy, fz;
+  int* nonfinite = nullptr;  // f32: device flag the kernel raises (vkt_capi.cu)
 };
 
 void set_error_detail(const char* fmt, ...);

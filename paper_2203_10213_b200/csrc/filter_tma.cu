@@ -11,6 +11,7 @@
 
 #include "dispatch.h"
 #include "filter_tma.cuh"
+#include "filter_sep.cuh"
 #include "filter_ws.cuh"
 
 namespace vkt {
@@ -72,17 +73,31 @@ extern template cudaError_t launch_ws_dtype<uint16_t>(int, const CUtensorMap&, c
                                                       const CUtensorMap&, const tma::TmaParams&,
                                                       const float*, dim3, cudaStream_t);
 }  // namespace tmaws
+namespace sep {
+#define VKT_SEP_DECL(T)                                                                            \
+  extern template cudaError_t launch_sep_dtype<T>(int, int, const CUtensorMap&, const CUtensorMap&, \
+                                                  const CUtensorMap&, const tma::TmaParams&,        \
+                                                  const float*, const float*, const float*, dim3,   \
+                                                  cudaStream_t);
+VKT_SEP_DECL(uint8_t)
+VKT_SEP_DECL(uint16_t)
+VKT_SEP_DECL(float)
+#undef VKT_SEP_DECL
+}  // namespace sep
 
 namespace {
 
 
 
-// u8/u16 3x3x3 run the warp-specialized kernel (filter_ws.cuh), with 32-row
-// tiles; everything else the paired-layout kernel's 16-row tiles.
-bool warp_kernel(const vkt_filter_args& a) {
-  return a.format != VKT_F32 && a.kdims.x == 3;
+// Separable plans run filter_sep.cuh; u8/u16 3x3x3 dense plans the
+// warp-specialized kernel (filter_ws.cuh), with 32-row tiles; everything else
+// the paired-layout kernel's 16-row tiles.
+bool warp_kernel(const FilterPlan& plan) {
+  return !plan.sep && plan.args->format != VKT_F32 && plan.args->kdims.x == 3;
 }
-int tile_rows(const vkt_filter_args& a) { return warp_kernel(a) ? tmaws::TY : tma::TY; }
+int tile_rows(const FilterPlan& plan) {
+  return plan.sep ? sep::tile_rows(plan.args->kdims.x) : warp_kernel(plan) ? tmaws::TY : tma::TY;
+}
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -135,14 +150,15 @@ int tma_chunk_planes(const FilterPlan& plan) {
   const int k = a.kdims.x, r = k / 2;
   const int nzo = plan.z_end - plan.z_begin;
   if (nzo <= 0) return 1;
-  const int ty = tile_rows(a);
+  const int ty = tile_rows(plan);
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + ty - 1) / ty);
   // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
   // K = 3 (4, Wrap 3)
-  const int64_t slots = (int64_t)sm_count() * (a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
+  const int64_t slots = (int64_t)sm_count() * (plan.sep ? sep::CTAS_PER_SM
+                                 : a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
                                  : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
-                                 : warp_kernel(a) ? tmaws::CTAS_PER_SM
+                                 : warp_kernel(plan) ? tmaws::CTAS_PER_SM
                                                   : tma::Layout<2, 3>::CTAS_PER_SM);
   // Under 3 waves the grid balances poorly: 512^3 u16 3^3 runs 0.266 ms at
   // 64-plane chunks (1.7 waves), 0.246 at 32 (3.5 waves); f32 3^3 0.241 vs
@@ -176,7 +192,7 @@ int tma_chunk_planes(const FilterPlan& plan) {
   // than the model's pick (1024^3 u16 / f32 7^3: 11.32 -> 11.11 ms,
   // profiles/r01_zc_sweep2_v36.txt); K <= 5 gains nothing measurable (~94-plane
   // chunks at 1024^3 K = 5: 4.261 vs 4.257 ms, profiles/r01_k5_chunks_v39.txt).
-  if (k >= 7) {
+  if (k >= 7 && !plan.sep) {
     const int nch = (nzo + 170) / 171;
     if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
   }
@@ -202,8 +218,8 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
                    const void* hhi, int pitch, cudaStream_t s) {
   const vkt_filter_args& a = *plan.args;
   const int k = a.kdims.x, r = k / 2;
-  const int ty = tile_rows(a);
-  const bool wk = warp_kernel(a);
+  const int ty = tile_rows(plan);
+  const bool wk = warp_kernel(plan);
   CUtensorMap ms, ml, mh;
   if (!encode(&ms, src, a.format, a.dims.x, a.dims.y, a.dims.z, r, pitch, ty)) return -1;
   ml = ms;
@@ -229,6 +245,7 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   p.yskip = plan.yskip;
   const bool aniso = plan.kxs > 0 && !wk && k >= 5;
   p.guard = plan.guard;
+  p.nonfinite = plan.nonfinite;
 
   const int nzo = plan.z_end - plan.z_begin;
   const int zc = tma_chunk_planes(plan);
@@ -237,7 +254,12 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
   if (grid.y > 65535 || grid.z > 65535) return -1;
 
   cudaError_t err;
-  switch (a.format) {
+  if (plan.sep) {
+    const float *fx = plan.fx.data(), *fy = plan.fy.data(), *fz = plan.fz.data();
+    err = a.format == VKT_U8    ? sep::launch_sep_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, fx, fy, fz, grid, s)
+          : a.format == VKT_U16 ? sep::launch_sep_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, fx, fy, fz, grid, s)
+                                : sep::launch_sep_dtype<float>(k, a.address_mode, ms, ml, mh, p, fx, fy, fz, grid, s);
+  } else switch (a.format) {
     case VKT_U8:
       err = wk      ? tmaws::launch_ws_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)
             : aniso ? tma::launch_tma_aniso<uint8_t>(k, plan.kxs, plan.zthin, a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)

@@ -169,6 +169,7 @@ struct TmaParams {
   uint32_t zskip;        // anisotropic kernels in a K^3 cube: bit dz set = padding plane,
   uint32_t yskip;        //   bit dy set = padding row (the x extent is a template)
   const int* guard;      // non-null: the launch does nothing when *guard != 0 (vkt_capi.cu)
+  int* nonfinite;        // separable f32 kernel: set to 1 when a stored output is Inf/NaN
 };
 
 // ---------------------------------------------------------------------------

@@ -239,6 +239,103 @@ static int launch_guarded(const FilterPlan& plan, FilterPlan& cube, cudaStream_t
   return st;
 }
 
+// Separable (rank-1) weights: W[z][y][x] = fz[z] * fy[y] * fx[x], checked in
+// float64 against the largest weight (gaussian_kernel is g(x)g(x)g over its
+// sum, box_kernel a constant: both factor to ~1 ulp).  Pivot on the largest
+// |W| so |fy|, |fx| <= 1 and fz carries the scale.  A tolerance of 1e-9 of
+// the largest weight is far below the f32 rounding of the weights
+// themselves (~6e-8 relative), which every tiled path already applies.
+static bool factor_rank1(const double* w, int kx, int ky, int kz, std::vector<double>& fx,
+                         std::vector<double>& fy, std::vector<double>& fz) {
+  const size_t n = (size_t)kx * ky * kz;
+  size_t piv = 0;
+  double mx = 0.0;
+  for (size_t i = 0; i < n; ++i)
+    if (std::fabs(w[i]) > mx) mx = std::fabs(w[i]), piv = i;
+  fx.assign(kx, 1.0);
+  fy.assign(ky, 1.0);
+  fz.assign(kz, 0.0);
+  if (mx == 0.0) return true;  // the zero kernel
+  const int px = (int)(piv % kx), py = (int)(piv / kx % ky), pz = (int)(piv / ((size_t)kx * ky));
+  auto at = [&](int z, int y, int x) { return w[((size_t)z * ky + y) * kx + x]; };
+  const double pv = at(pz, py, px);
+  for (int z = 0; z < kz; ++z) fz[z] = at(z, py, px);
+  for (int y = 0; y < ky; ++y) fy[y] = at(pz, y, px) / pv;
+  for (int x = 0; x < kx; ++x) fx[x] = at(pz, py, x) / pv;
+  const double tol = 1e-9 * mx;
+  for (int z = 0; z < kz; ++z)
+    for (int y = 0; y < ky; ++y)
+      for (int x = 0; x < kx; ++x)
+        if (!(std::fabs(at(z, y, x) - fz[z] * fy[y] * fx[x]) <= tol)) return false;
+  return true;
+}
+
+// The separable plan (filter_sep.cuh) for a validated plan, or false.
+// Integer voxels at every K in {3,5,7,9}; f32 from K = 5 (f32 3^3 is
+// HBM-bound on the dense kernel already).  Anisotropic kernels pad their
+// factors with zeros to the K^3 cube (z only when unsharded, as pad_to_cube).
+// `cube` receives the cube's args (weights NULL: the plan carries factors).
+static bool plan_separable(const FilterPlan& plan, vkt_filter_args& cube, FilterPlan& sp) {
+  const vkt_filter_args* a = plan.args;
+  if (a->flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT | VKT_FLAG_NO_SEPARABLE)) return false;
+  const int kx = a->kdims.x, ky = a->kdims.y, kz = a->kdims.z;
+  int k = kx > ky ? kx : ky;
+  k = k > kz ? k : kz;
+  if (k != 3 && k != 5 && k != 7 && k != 9) return false;
+  if (a->format == VKT_F32 && k == 3) return false;
+  const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
+                         (a->global_nz <= 0 || a->global_nz == a->dims.z);
+  if (kz != k && !unsharded) return false;
+  std::vector<double> fx, fy, fz;
+  if (!factor_rank1(a->weights, kx, ky, kz, fx, fy, fz)) return false;
+  cube = *a;
+  cube.kdims = vkt_int3{k, k, k};
+  cube.weights = nullptr;
+  if (!tma_supported(cube)) return false;
+  sp = plan;
+  sp.args = &cube;
+  sp.path = VKT_PATH_SEPARABLE;
+  sp.sep = true;
+  sp.geom.rz = k / 2;
+  auto pad = [k](const std::vector<double>& f, std::vector<float>& out) {
+    out.assign(k, 0.0f);
+    const int o = (k - (int)f.size()) / 2;
+    for (size_t i = 0; i < f.size(); ++i) out[o + i] = (float)f[i];
+  };
+  pad(fx, sp.fx);
+  pad(fy, sp.fy);
+  pad(fz, sp.fz);
+  return true;
+}
+
+// The separable launch.  f32: the kernel raises a device flag when a stored
+// output is Inf/NaN (an Inf/NaN input in its window), and the direct kernel,
+// guarded by that flag, then recomputes the launch's outputs with the dense
+// arithmetic (it does nothing otherwise).  Returns -1 when the tiled kernel
+// does not cover the plan.
+static int launch_separable(const FilterPlan& plan, FilterPlan& sp, cudaStream_t s) {
+  if (plan.args->format != VKT_F32) return launch_filter_tma(sp, s);
+  void* flag = nullptr;
+  cudaError_t err = scratch_alloc(&flag, sizeof(int), s);
+  if (err != cudaSuccess) {
+    set_error_detail("scratch_alloc(flag): %s", cudaGetErrorString(err));
+    return err == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
+  }
+  int st = cudaMemsetAsync(flag, 0, sizeof(int), s) == cudaSuccess ? VKT_OK : VKT_DEVICE_FAILURE;
+  if (st != VKT_OK) set_error_detail("flag memset: %s", cudaGetErrorString(cudaGetLastError()));
+  if (st == VKT_OK) {
+    sp.nonfinite = static_cast<int*>(flag);
+    st = launch_filter_tma(sp, s);
+    if (st == VKT_OK) {
+      FilterPlan direct = plan;
+      direct.guard = static_cast<const int*>(flag);
+      st = launch_filter_direct(direct, s);
+    }
+  }
+  scratch_free(flag, s);
+  return st;
+}
+
 }  // namespace vkt
 
 using namespace vkt;
@@ -250,6 +347,14 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
   FilterPlan plan;
   int st = validate_and_plan(args, plan);
   if (st != VKT_OK) return st;
+  if (plan.z_end > plan.z_begin) {
+    vkt_filter_args cube;
+    FilterPlan sp;
+    if (plan_separable(plan, cube, sp)) {
+      const int st2 = launch_separable(plan, sp, reinterpret_cast<cudaStream_t>(stream));
+      if (st2 != -1) return st2;
+    }
+  }
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;
@@ -282,6 +387,11 @@ int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
 int vkt_filter_path(const vkt_filter_args* args) {
   FilterPlan plan;
   if (validate_and_plan(args, plan) != VKT_OK) return VKT_PATH_NONE;
+  {
+    vkt_filter_args sc;
+    FilterPlan sp;
+    if (plan_separable(plan, sc, sp)) return VKT_PATH_SEPARABLE;
+  }
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;
@@ -296,6 +406,11 @@ int vkt_filter_path(const vkt_filter_args* args) {
 int vkt_filter_chunk_planes(const vkt_filter_args* args) {
   FilterPlan plan;
   if (validate_and_plan(args, plan) != VKT_OK) return 0;
+  {
+    vkt_filter_args sc;
+    FilterPlan sp;
+    if (plan_separable(plan, sc, sp)) return tma_chunk_planes(sp);
+  }
   if (plan.path == VKT_PATH_DIRECT) {
     vkt_filter_args cube;
     std::vector<double> wcube;

@@ -41,7 +41,8 @@ class Device(Enum):
 
 
 class FilterPath(Enum):
-    AUTO = "auto"      # tiled TMA kernel when it applies, else direct
+    AUTO = "auto"      # separable kernel for rank-1 weights, else dense tiled, else direct
+    DENSE = "dense"    # as AUTO without the separable kernel (bit-identical to DIRECT)
     DIRECT = "direct"  # generic one-output-per-thread kernel
     EXACT = "exact"    # float64, bit-exact with the reference arithmetic
 

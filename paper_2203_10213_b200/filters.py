@@ -132,6 +132,8 @@ def _flags(policy) -> int:
         return _capi.FLAG_EXACT_F64
     if policy.filter_path is FilterPath.DIRECT:
         return _capi.FLAG_FORCE_DIRECT
+    if policy.filter_path is FilterPath.DENSE:
+        return _capi.FLAG_NO_SEPARABLE
     return 0
 
 
@@ -168,7 +170,8 @@ def launch(args, stream_handle: int) -> None:
 
 def filter_path(dst: StructuredVolume, src: StructuredVolume, kernel: Kernel,
                 address_mode=AddressMode.CLAMP) -> str:
-    """Which kernel ApplyFilter would launch ("tma", "direct", "exact")."""
+    """Which kernel ApplyFilter would launch ("separable", "tma", "direct",
+    "exact")."""
     mode = AddressMode.coerce(address_mode)
     args, _keep = make_args(dst.data_ptr(), src.data_ptr(), src.dims, src.format, src.mapping,
                             kernel, mode, flags=_flags(get_execution_policy()))

@@ -153,9 +153,9 @@ def test_cfg3_1024_u16_gauss7_clamp_bench_launch():
     k = vk.gaussian_kernel(1.5)
     assert k.dims == (7, 7, 7)
     vk.ApplyFilter(dst, src, k, vk.AddressMode.CLAMP)
-    assert vk.filter_path(dst, src, k) == "tma"
+    assert vk.filter_path(dst, src, k) == "separable"  # gaussian_kernel is rank-1
     zc = vk.chunk_planes(src, k)
-    assert 150 <= zc <= 200, zc  # the deep-chunk rule: ~171-plane chunks at 1024^3, K = 7
+    assert 0 < zc <= 64, zc
     ranges = [(0, 4), (1020, 1024)] + boundary_ranges(zc, 1024)
     reps = check_ranges("cfg3", src, dst, k.weights, "clamp", ranges)
     assert max(r["max_lsb"] for r in reps) <= 1

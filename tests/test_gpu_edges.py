@@ -104,8 +104,15 @@ def test_anisotropic_integer_kernels_on_the_tiled_path(kd, fmt):
     w /= w.sum()
     src = vk.StructuredVolume.from_numpy(stored, FMT[fmt])
     dst = vk.StructuredVolume(src.dims, src.format)
-    assert vk.filter_path(dst, src, vk.Kernel(kd, w.reshape(-1))) == "tma"
     kernel = vk.Kernel(kd, w.reshape(-1))
+    # a 1-D kernel is rank-1 and takes the separable kernel under "auto"
+    auto = "separable" if sum(d > 1 for d in kd) == 1 else "tma"
+    assert vk.filter_path(dst, src, kernel) == auto
+    vk.set_execution_policy(vk.ExecutionPolicy(filter_path="dense"))
+    try:
+        assert vk.filter_path(dst, src, kernel) == "tma"
+    finally:
+        vk.set_execution_policy(vk.ExecutionPolicy())
 
     def run(mode, path):
         vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
@@ -117,9 +124,10 @@ def test_anisotropic_integer_kernels_on_the_tiled_path(kd, fmt):
 
     for mode in ("wrap", "mirror", "clamp", "border"):
         want = O.apply_filter(stored, fmt, w, mode, workers=1)
-        got = run(mode, "auto")
-        ok, ndiff, dmax = within_contract(got, want, fmt, w)
-        assert ok, (kd, mode, ndiff, dmax)
+        for path in ("auto", "dense"):
+            got = run(mode, path)
+            ok, ndiff, dmax = within_contract(got, want, fmt, w)
+            assert ok, (kd, mode, path, ndiff, dmax)
         assert np.array_equal(got, run(mode, "direct")), (kd, mode)
 
 
@@ -184,17 +192,24 @@ def test_anisotropic_f32_cube(kd, nx):
             vk.set_execution_policy(vk.ExecutionPolicy())
 
     src = vk.StructuredVolume.from_numpy(finite, vk.DataFormat.FLOAT32)
-    assert vk.filter_path(dst, src, kernel) == "tma"
+    # 1-D kernels with K >= 5 are rank-1: the separable kernel under "auto"
+    # (within contract; Inf / NaN inputs fall back to the direct kernel)
+    sep = sum(d > 1 for d in kd) == 1 and max(kd) >= 5
+    assert vk.filter_path(dst, src, kernel) == ("separable" if sep else "tma")
     bad = finite.copy()
     bad[4, 10, 70] = np.inf
     bad[2, 5, 3] = np.nan
     for mode in ("wrap", "mirror", "clamp", "border"):
-        got = run(finite, mode, "auto")
+        want = O.apply_filter(finite, 3, w, mode, workers=1)
+        got = run(finite, mode, "dense")
         assert np.array_equal(got, run(finite, mode, "direct")), (kd, mode)
-        ok, ndiff, dmax = within_contract(got, O.apply_filter(finite, 3, w, mode, workers=1), 3, w)
+        ok, ndiff, dmax = within_contract(got, want, 3, w)
         assert ok, (kd, mode, ndiff, dmax)
-        got = run(bad, mode, "auto")
-        assert np.array_equal(got.view(np.uint32), run(bad, mode, "direct").view(np.uint32)), (kd, mode)
+        ok, ndiff, dmax = within_contract(run(finite, mode, "auto"), want, 3, w)
+        assert ok, (kd, mode, "auto", ndiff, dmax)
+        direct_bad = run(bad, mode, "direct").view(np.uint32)
+        for path in ("auto", "dense"):
+            assert np.array_equal(run(bad, mode, path).view(np.uint32), direct_bad), (kd, mode, path)
 
 
 @pytest.mark.parametrize("zc", [171, 200, 397])

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 for c in "$@"; do
   set -- $c
   name="${tag}_$1k$2$3_$4_$5"
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"filter_(tma|warp|ws)" -c 1 \
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"filter_(tma|warp|ws|sep)" -c 1 \
     -o gpurun_out/$name -f python tools/profile_case.py --fmt $1 --k $2 --kernel $3 --mode $4 --n $5 --reps 1 \
     > gpurun_out/$name.log 2>&1
 done

@@ -14,27 +14,28 @@
 // kernels, whose (dz, dy, dx) sums round differently.
 //
 // Layout.  A CTA owns TX = 128 x outputs by TY rows and a chunk of ZC output
-// planes, and streams the chunk's input planes (TMA 3D box per plane, with
-// its halo, into a raw ring) through two passes per plane:
-//  * x pass: every thread widens quads of raw cells into (x, x+64) float
-//    pairs (the paired layout of filter_tma.cuh: one FFMA2 advances two
-//    outputs with one broadcast weight) and writes the row's K-tap x sums for
-//    8 outputs (4 pairs) into a double-buffered float-pair plane `xb`
-//    (TY + 2R rows x 64 pairs);
-//  * y + z pass: each thread owns one pair column of YPT rows: it reads the
-//    YPT + 2R x sums of its column from xb (one LDS.64 each), forms the YPT
-//    y sums, and folds them into K rolling z accumulators per output (the
-//    partial sums of the K output planes this input plane reaches).  The
-//    roll happens inside the FMAs: slot m takes slot m+1's sum plus this
-//    plane's tap (tma::ffma2_from), so there is no register move.
-// One CTA barrier per plane: iteration j runs the x pass of plane j, the
-// y + z pass of plane j-1 (the other xb buffer), and repairs plane j+1's
-// out-of-volume cells in its raw slot (edge tiles, Clamp / Mirror / Wrap)
-// once TMA has delivered it; after the barrier, thread 0 refills plane j's
-// raw slot.  Border needs no repair: TMA fills out-of-bounds cells with
-// zeros (stored 0), and a Border plane outside the volume in z is fetched as
-// a fully out-of-bounds box.
-//
+// planes, and streams the chunk's input planes (one TMA 3D box per plane,
+// with its halo, into a raw ring) through two passes, on split warp roles
+// (as filter_ws.cuh) that meet only on mbarriers:
+//  * PW producer warps wait for a plane's box, repair its out-of-volume cells
+//    (edge tiles, Clamp / Mirror / Wrap; Border is TMA's zero fill, and a
+//    Border plane outside the volume in z a fully out-of-bounds box), then
+//    run the x pass: widen quads of raw cells into (x, x+64) float pairs (the
+//    paired layout of filter_tma.cuh: one FFMA2 advances two outputs with one
+//    broadcast weight) and write each row's K-tap x sums for 8 outputs
+//    (4 pairs) into a ring of float-pair planes `xb` (TY + 2R rows x 64
+//    pairs; 16-byte chunks XOR-swizzled so the producers' STS.128 and the
+//    consumers' LDS.64 are conflict-free).  The first producer refills the
+//    raw slot once every producer has read it (named barrier).
+//  * CW consumer warps each own one pair column of YPT rows: they read the
+//    YPT + 2R x sums of their column (one LDS.64 each), form the YPT y sums
+//    and fold them into K z accumulators per output -- the partial sums of
+//    the K output planes this input plane reaches.  The plane loop is
+//    unrolled by K and the accumulators rotate by NAME: at plane phase phi,
+//    logical slot m lives in register (m + phi) % K, so every z tap is an
+//    in-place FFMA2 (no register moves; a rolled loop costs ~10% extra
+//    instructions in moves) and the completed slot is stored from register
+//    phi.
 // Non-finite f32 inputs: the dense kernels evaluate 0 * Inf = NaN exactly
 // where the reference does; a factored sum may not (and padded anisotropic
 // factors hold zeros).  Every stored output whose window holds an Inf or NaN
@@ -53,23 +54,24 @@ using tma::TmaParams;
 
 constexpr int TX = tma::TX;
 constexpr int HALF = tma::HALF;
-constexpr int THREADS = 256;
-constexpr int WARPS = THREADS / 32;
+constexpr int CW = 8;                   // consumer warps: 4 row groups x 64 pair columns
+constexpr int PW = 4;                   // producer warps
+constexpr int THREADS = 32 * (CW + PW);
 constexpr int CTAS_PER_SM = 2;
 constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 
 template <int K>
 struct Shape {
   static constexpr int R = K / 2;
-  static constexpr int YPT = K == 3 ? 8 : 4;  // y + z pass rows per thread
-  static constexpr int RG = WARPS / 2;        // row groups: 2 warps (64 pairs) each
-  static constexpr int TY = RG * YPT;
+  static constexpr int YPT = K == 3 ? 8 : K == 9 ? 3 : 4;  // consumer rows per thread
+  static constexpr int TY = (CW / 2) * YPT;   // 2 consumer warps (64 pair columns) per row group
   static constexpr int BY = TY + 2 * R;       // raw / x-sum rows
   static constexpr int NQ = BY * GPR;         // x-pass items per plane
-  static constexpr int QPT = (NQ + THREADS - 1) / THREADS;
+  static constexpr int PT = 32 * PW;          // producer threads
+  static constexpr int QPT = (NQ + PT - 1) / PT;
 };
 
-__host__ __device__ constexpr int tile_rows(int k) { return (WARPS / 2) * (k == 3 ? 8 : 4); }
+__host__ __device__ constexpr int tile_rows(int k) { return (CW / 2) * (k == 3 ? 8 : k == 9 ? 3 : 4); }
 
 template <typename T, int K>
 struct Cfg {
@@ -79,10 +81,11 @@ struct Cfg {
   static constexpr int RAW_BYTES = BX * S::BY * (int)sizeof(T);
   static constexpr int RAW_PITCH = (RAW_BYTES + 127) / 128 * 128;
   static constexpr int XB_BYTES = S::BY * HALF * 8;
+  static constexpr int SX = 3;  // x-sum stages
   static constexpr int SMEM_PER_CTA = (228 * 1024) / CTAS_PER_SM - 1024;
-  static constexpr int FIT = (SMEM_PER_CTA - 256 - 2 * XB_BYTES) / RAW_PITCH;
+  static constexpr int FIT = (SMEM_PER_CTA - 512 - SX * XB_BYTES) / RAW_PITCH;
   static constexpr int S_RAW = FIT < 8 ? FIT : 8;
-  static constexpr int SMEM = 2 * XB_BYTES + S_RAW * RAW_PITCH + S_RAW * 8 + 128;
+  static constexpr int SMEM = SX * XB_BYTES + S_RAW * RAW_PITCH + (S_RAW + 2 * SX) * 8 + 128;
   static_assert(S_RAW >= 4, "TMA ring too shallow");
   static_assert(SMEM <= SMEM_PER_CTA, "shared memory budget");
   static_assert(BX <= 256 && S::BY <= 256, "TMA box too large");
@@ -114,6 +117,11 @@ __device__ __forceinline__ uint32_t sat_floor(float v) {
   return d;
 }
 
+// Physical 16-byte chunk of logical chunk ci (2 pairs) in an xb row: odd
+// halves of each 16-chunk group swap neighbours, so the 8 lanes of a
+// producer's STS.128 phase (chunks 2g, g = 0..7) hit 8 distinct bank groups.
+__device__ __forceinline__ int xb_chunk(int ci) { return ci ^ ((ci >> 3) & 1); }
+
 template <typename T, int K, int MODE>
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
     filter_sep_kernel(const __grid_constant__ CUtensorMap map_src,
@@ -122,12 +130,15 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
                       const __grid_constant__ Factors<K> f) {
   using C = Cfg<T, K>;
   using S = Shape<K>;
-  constexpr int R = S::R, YPT = S::YPT, TY = S::TY, BY = S::BY, SR = C::S_RAW;
+  constexpr int R = S::R, YPT = S::YPT, TY = S::TY, BY = S::BY, SR = C::S_RAW, SX = C::SX;
+  constexpr int PT = S::PT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (tma::smem_u32(smem_raw) & 127u)) & 127u);
   T* raw_base = reinterpret_cast<T*>(smem);
   uint64_t* xb_base = reinterpret_cast<uint64_t*>(smem + SR * C::RAW_PITCH);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SR * C::RAW_PITCH + 2 * C::XB_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SR * C::RAW_PITCH + SX * C::XB_BYTES);
+  uint64_t* ready = full + SR;  // [SX] producers done writing (PW arrivals)
+  uint64_t* empty = ready + SX; // [SX] consumers done reading (CW arrivals)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -142,51 +153,121 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   if (tid == 0) {
     tma::prefetch_tmap(&map_src);
     for (int s = 0; s < SR; ++s) tma::mbar_init(&full[s], 1);
+    for (int s = 0; s < SX; ++s) {
+      tma::mbar_init(&ready[s], PW);
+      tma::mbar_init(&empty[s], CW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  const bool leader = tid == 0;
-  auto raw_slot = [&](int r) { return raw_base + r * (C::RAW_PITCH / (int)sizeof(T)); };
-  auto issue = [&](int j, int r) {  // input plane j into raw slot r
-    const tma::PlaneSrc s = tma::resolve<MODE>(p, R, zo0 - R + j);
-    const CUtensorMap* m = s.which <= 0 ? &map_src : s.which == 1 ? &map_lo : &map_hi;
-    tma::tma_issue_if(raw_slot(r), m, &full[r], C::RAW_BYTES, x0 - C::A, y0 - R,
-                      s.which < 0 ? -1 : s.z, leader);
-  };
-  for (int j = 0; j < SR && j < np; ++j) issue(j, j);
+  if (warp >= CW) {
+    // ---------------------------------------------------------------- producer
+    const int pt = tid - 32 * CW;
+    const bool leader = pt == 0;
+    auto raw_slot = [&](int r) { return raw_base + r * (C::RAW_PITCH / (int)sizeof(T)); };
+    auto issue = [&](int j, int r) {  // input plane j into raw slot r
+      const tma::PlaneSrc s = tma::resolve<MODE>(p, R, zo0 - R + j);
+      const CUtensorMap* m = s.which <= 0 ? &map_src : s.which == 1 ? &map_lo : &map_hi;
+      tma::tma_issue_if(raw_slot(r), m, &full[r], C::RAW_BYTES, x0 - C::A, y0 - R,
+                        s.which < 0 ? -1 : s.z, leader);
+    };
+    for (int j = 0; j < SR && j < np; ++j) issue(j, j);
 
-  // out-of-volume cells of the read window (edge tiles; Clamp / Mirror / Wrap)
-  const int ya = y0 - R;
-  const int yb = min(y0 + TY, p.ny) + R;
-  const int xb_end = min(x0 + TX, p.nx) + R;
-  const bool edge = MODE != VKT_BORDER && (x0 - R < 0 || xb_end > p.nx || ya < 0 || yb > p.ny);
-  const tmaws::EdgeCells ec(p.nx, p.ny, x0 - R, xb_end, ya, edge ? yb : ya);
-  auto repair = [&](int j, T* raw) {
-    if constexpr (MODE != VKT_BORDER) {
-      if (!edge) return;
-      const tma::PlaneSrc src = tma::resolve<MODE>(p, R, zo0 - R + j);
-      for (int q = tid; q < ec.total; q += THREADS) {
-        int gx, gy;
-        ec.cell(p.nx, p.ny, q, gx, gy);
-        // the full mapping: a volume thinner than the halo overshoots by more
-        // than one extent (the mapped cell is inside the box: the tile then
-        // covers the whole axis)
-        const int mx = (int)map_index<MODE>(gx, p.nx), my = (int)map_index<MODE>(gy, p.ny);
-        T v;
-        if constexpr (MODE == VKT_WRAP)
-          v = __ldg(tma::plane_ptr<T>(p, src) + (int64_t)my * p.pitch + mx);
-        else
-          v = raw[(my - ya) * C::BX + mx - (x0 - C::A)];
-        VKT_CHECK((gy - ya) * C::BX + gx - (x0 - C::A) >= 0 &&
-                      (gy - ya) * C::BX + gx - (x0 - C::A) < C::BX * BY,
-                  "sep repair: dest");
-        raw[(gy - ya) * C::BX + gx - (x0 - C::A)] = v;
+    // out-of-volume cells of the read window (edge tiles; Clamp / Mirror / Wrap)
+    const int ya = y0 - R;
+    const int yb = min(y0 + TY, p.ny) + R;
+    const int xb_end = min(x0 + TX, p.nx) + R;
+    const bool edge = MODE != VKT_BORDER && (x0 - R < 0 || xb_end > p.nx || ya < 0 || yb > p.ny);
+    const tmaws::EdgeCells ec(p.nx, p.ny, x0 - R, xb_end, ya, edge ? yb : ya);
+
+    // this thread's x-pass items: g fixed (pt & 15), rows pt/16 + (PT/16)*k
+    const int g = pt & (GPR - 1);
+    const int row0 = pt / GPR;
+    const int b = (g >> 2) & 1;
+    const int src_off = row0 * C::BX + (C::A - 4) + 4 * g;    // + k * (PT/GPR) * BX
+    const int dst_off0 = row0 * HALF + 2 * ((2 * g) ^ b);       // in pairs, + k * (PT/GPR) * HALF
+    const int dst_off1 = row0 * HALF + 2 * ((2 * g + 1) ^ b);
+    const uint64_t zero2 = tma::f2pack(0.0f, 0.0f);
+
+    int r = 0, s = 0;
+    uint32_t rph = 0, sph = 0;
+#pragma unroll 1
+    for (int j = 0; j < np; ++j) {
+      T* raw = raw_slot(r);
+      VKT_JITTER_POINT(4 * j);
+      tma::mbar_wait(&full[r], rph);
+      if constexpr (MODE != VKT_BORDER) {
+        if (edge) {
+          const tma::PlaneSrc src = tma::resolve<MODE>(p, R, zo0 - R + j);
+          for (int q = pt; q < ec.total; q += PT) {
+            int gx, gy;
+            ec.cell(p.nx, p.ny, q, gx, gy);
+            // the full mapping: a volume thinner than the halo overshoots by
+            // more than one extent (the mapped cell is still in the box: the
+            // tile then covers the whole axis)
+            const int mx = (int)map_index<MODE>(gx, p.nx), my = (int)map_index<MODE>(gy, p.ny);
+            T v;
+            if constexpr (MODE == VKT_WRAP)
+              v = __ldg(tma::plane_ptr<T>(p, src) + (int64_t)my * p.pitch + mx);
+            else
+              v = raw[(my - ya) * C::BX + mx - (x0 - C::A)];
+            const int d = (gy - ya) * C::BX + gx - (x0 - C::A);
+            VKT_CHECK(d >= 0 && d < C::BX * BY, "sep repair: dest");
+            raw[d] = v;
+          }
+          tma::fence_proxy_async();
+          asm volatile("bar.sync 1, %0;" ::"r"(PT) : "memory");
+        }
       }
+      if (j >= SX) tma::mbar_wait(&empty[s], sph ^ 1u);
+      uint64_t* xb = xb_base + s * (C::XB_BYTES / 8);
+#pragma unroll
+      for (int k = 0; k < S::QPT; ++k) {
+        if (S::NQ % PT != 0 && k == S::QPT - 1 && pt + PT * k >= S::NQ) break;
+        // cells x0-4+4g .. x0+4g+7 (and +HALF): output pair jj at tap dx
+        // reads cell 4g + jj + dx - R, i.e. index jj + dx + 4 - R here
+        const T* src = raw + src_off + k * (PT / GPR) * C::BX;
+        uint64_t P[12];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          uint32_t lo[4], hi[4];
+          tma::load_quad<T>(src + 4 * i, lo);
+          tma::load_quad<T>(src + 4 * i + HALF, hi);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (4 * i + e < 4 - R || 4 * i + e >= 8 + R) continue;
+            if constexpr (sizeof(T) == 4)
+              P[4 * i + e] = (uint64_t)lo[e] | ((uint64_t)hi[e] << 32);
+            else
+              P[4 * i + e] = tma::widen2(lo[e], hi[e]);
+          }
+        }
+        uint64_t o[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          o[jj] = tma::ffma2_from(P[jj + 4 - R], f.wx[0], zero2);
+#pragma unroll
+          for (int dx = 1; dx < K; ++dx) tma::ffma2_bw(P[jj + dx + 4 - R], f.wx[dx], o[jj]);
+        }
+        uint64_t* d = xb + k * (PT / GPR) * HALF;
+        *reinterpret_cast<uint4*>(d + dst_off0) =
+            make_uint4((uint32_t)o[0], (uint32_t)(o[0] >> 32), (uint32_t)o[1], (uint32_t)(o[1] >> 32));
+        *reinterpret_cast<uint4*>(d + dst_off1) =
+            make_uint4((uint32_t)o[2], (uint32_t)(o[2] >> 32), (uint32_t)o[3], (uint32_t)(o[3] >> 32));
+      }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&ready[s]);
+      // every producer has read raw slot r: the first one refills it
+      asm volatile("bar.sync 1, %0;" ::"r"(PT) : "memory");
+      if (j + SR < np) issue(j + SR, r);
+      if (++r == SR) r = 0, rph ^= 1u;
+      if (++s == SX) s = 0, sph ^= 1u;
     }
-  };
+    return;
+  }
 
-  // y + z pass: pair column c of rows [rg*YPT, rg*YPT + YPT)
+  // ---------------------------------------------------------------- consumer
   const int rg = warp >> 1;
   const int c = 32 * (warp & 1) + lane;
   const float a0 = acc_init<T>(p.c);
@@ -204,64 +285,19 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   const int rows_ok = min(YPT, p.ny - oy);
   const int64_t plane_elems = (int64_t)p.pitch * p.ny;
   T* out_plane = static_cast<T*>(p.dst) + (int64_t)oy * p.pitch + ox + (int64_t)zo0 * plane_elems;
+  const int col_off = rg * YPT * HALF + 2 * xb_chunk(c >> 1) + (c & 1);
 
-  // plane 0 in place and repaired before the loop
-  tma::mbar_wait(&full[0], 0);
-  repair(0, raw_slot(0));
-  if (edge) tma::fence_proxy_async();
-  __syncthreads();
-
-  int r = 0;
-  uint32_t ph = 0;
+  int s = 0;
+  uint32_t sph = 0;
 #pragma unroll 1
-  for (int j = 0; j <= np; ++j) {
-    VKT_JITTER_POINT(j);
-    if (j < np) {
-      // ---- x pass: raw slot r -> xb[j & 1]
-      const T* raw = raw_slot(r);
-      uint64_t* xb = xb_base + (j & 1) * (C::XB_BYTES / 8);
+  for (int jb = 0; jb < np; jb += K) {
 #pragma unroll
-      for (int k = 0; k < S::QPT; ++k) {
-        const int q = tid + THREADS * k;
-        if (S::NQ % THREADS != 0 && k == S::QPT - 1 && q >= S::NQ) break;
-        const int row = q / GPR, g = q - row * GPR;
-        // cells x0-4+4g .. x0+4g+7 (and +HALF): output pair jj at tap dx
-        // reads cell 4g + jj + dx - R, i.e. index jj + dx + 4 - R here
-        const T* src = raw + row * C::BX + (C::A - 4) + 4 * g;
-        uint64_t P[12];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          uint32_t lo[4], hi[4];
-          tma::load_quad<T>(src + 4 * i, lo);
-          tma::load_quad<T>(src + 4 * i + HALF, hi);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if constexpr (sizeof(T) == 4)
-              P[4 * i + e] = (uint64_t)lo[e] | ((uint64_t)hi[e] << 32);
-            else
-              P[4 * i + e] = tma::widen2(lo[e], hi[e]);
-          }
-        }
-        uint64_t o[4];
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          o[jj] = tma::ffma2_from(P[jj + 4 - R], f.wx[0], zero2);
-#pragma unroll
-          for (int dx = 1; dx < K; ++dx) tma::ffma2_bw(P[jj + dx + 4 - R], f.wx[dx], o[jj]);
-        }
-        // two 16-byte chunks; odd quads of 4 lanes store their second chunk
-        // first so the 8 lanes of a phase cover all 32 banks
-        uint4 c0 = make_uint4((uint32_t)o[0], (uint32_t)(o[0] >> 32), (uint32_t)o[1], (uint32_t)(o[1] >> 32));
-        uint4 c1 = make_uint4((uint32_t)o[2], (uint32_t)(o[2] >> 32), (uint32_t)o[3], (uint32_t)(o[3] >> 32));
-        const bool swap = (lane >> 2) & 1;
-        uint4* d = reinterpret_cast<uint4*>(xb + row * HALF + 4 * g);
-        d[swap ? 1 : 0] = swap ? c1 : c0;
-        d[swap ? 0 : 1] = swap ? c0 : c1;
-      }
-    }
-    if (j >= 1) {
-      // ---- y + z pass on plane j-1 (xb[(j-1) & 1])
-      const uint64_t* col = xb_base + ((j - 1) & 1) * (C::XB_BYTES / 8) + rg * YPT * HALF + c;
+    for (int phi = 0; phi < K; ++phi) {
+      const int j = jb + phi;
+      if (j >= np) break;
+      VKT_JITTER_POINT(4 * j + 1);
+      tma::mbar_wait(&ready[s], sph);
+      const uint64_t* col = xb_base + s * (C::XB_BYTES / 8) + col_off;
       uint64_t ys[YPT];
 #pragma unroll
       for (int i = 0; i < YPT + 2 * R; ++i) {
@@ -274,41 +310,36 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
           else tma::ffma2_bw(v, f.wy[dy], ys[rr]);
         }
       }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[s]);
+      if (++s == SX) s = 0, sph ^= 1u;
+      // logical slot m (the output plane this input plane reaches with
+      // dz = K-1-m) lives in register (m + phi) % K
 #pragma unroll
-      for (int rr = 0; rr < YPT; ++rr)
+      for (int rr = 0; rr < YPT; ++rr) {
 #pragma unroll
-        for (int m = 0; m < K; ++m)
-          acc[rr][m] = tma::ffma2_from(ys[rr], f.wz[K - 1 - m], m + 1 < K ? acc[rr][m + 1 < K ? m + 1 : m] : a00);
-      if (j - 1 >= 2 * R) {
+        for (int m = 0; m < K - 1; ++m) tma::ffma2_bw(ys[rr], f.wz[K - 1 - m], acc[rr][(m + phi) % K]);
+        acc[rr][(K - 1 + phi) % K] = tma::ffma2_from(ys[rr], f.wz[0], a00);
+      }
+      VKT_JITTER_POINT(4 * j + 3);
+      if (j >= 2 * R) {
         T* o = out_plane;
 #pragma unroll
         for (int rr = 0; rr < YPT; ++rr, o += p.pitch) {
           if (rr >= rows_ok) continue;
+          const uint64_t v = acc[rr][phi];
           if constexpr (sizeof(T) == 4) {
-            chk = tma::ffma2_from(acc[rr][0], 0.0f, chk);
-            if (st_lo) st_cs(o, tma::f2lo(acc[rr][0]));
-            if (st_hi) st_cs(o + HALF, tma::f2hi(acc[rr][0]));
+            chk = tma::ffma2_from(v, 0.0f, chk);
+            if (st_lo) st_cs(o, tma::f2lo(v));
+            if (st_hi) st_cs(o + HALF, tma::f2hi(v));
           } else {
-            if (st_lo) st_cs(o, sat_floor<T>(tma::f2lo(acc[rr][0])));
-            if (st_hi) st_cs(o + HALF, sat_floor<T>(tma::f2hi(acc[rr][0])));
+            if (st_lo) st_cs(o, sat_floor<T>(tma::f2lo(v)));
+            if (st_hi) st_cs(o + HALF, sat_floor<T>(tma::f2hi(v)));
           }
         }
         out_plane += plane_elems;
       }
     }
-    // ---- plane j+1: wait for its TMA box, repair its out-of-volume cells
-    const int r1 = r + 1 == SR ? 0 : r + 1;
-    const uint32_t ph1 = r1 == 0 ? ph ^ 1u : ph;
-    if (j + 1 < np) {
-      tma::mbar_wait(&full[r1], ph1);
-      repair(j + 1, raw_slot(r1));
-      if (edge) tma::fence_proxy_async();
-    }
-    __syncthreads();
-    // every thread is past plane j's x pass: refill its raw slot
-    if (j < np && j + SR < np) issue(j + SR, r);
-    r = r1;
-    ph = ph1;
   }
   if constexpr (sizeof(T) == 4) {
     if (p.nonfinite != nullptr && (isnan(tma::f2lo(chk)) || isnan(tma::f2hi(chk)))) *p.nonfinite = 1;
@@ -355,7 +386,9 @@ cudaError_t launch_sep_dtype(int k, int mode, const CUtensorMap& ms, const CUten
       case VKT_BORDER: return launch_sep_kernel<T, KK, VKT_BORDER>(ms, ml, mh, p, fx, fy, fz, grid, s); \
       default: return cudaErrorInvalidValue;                                                         \
     }
-  VKT_SEP_CASES(3)
+  if constexpr (sizeof(T) != 4) {  // f32 3^3 runs the dense kernel (vkt_capi.cu)
+    VKT_SEP_CASES(3)
+  }
   VKT_SEP_CASES(5)
   VKT_SEP_CASES(7)
   VKT_SEP_CASES(9)

@@ -9,6 +9,8 @@
 // kernels needing x/y padding, f32 volumes with Inf/NaN under the guarded cube
 // path -- vkt_capi.cu pads the other anisotropic ones to a cube) and the
 // EXACT_F64 parity mode.
+#include <algorithm>
+
 #include "common.cuh"
 #include "dispatch.h"
 
@@ -110,6 +112,14 @@ static cudaError_t launch_direct_t(const DirectParams& p, bool exact, cudaStream
   dim3 block(32, 8, 1);
   int nzo = p.z_end - p.z_begin;
   dim3 grid((p.nx + 31) / 32, (p.ny + 7) / 8, (unsigned)(nzo < 65535 ? nzo : 65535));
+  // A guarded launch (the fallback behind a device flag, vkt_capi.cu) almost
+  // always does nothing: keep its grid to ~8 CTAs per SM (the kernel strides
+  // over z), so the no-op costs microseconds, not a pass over the volume.
+  if (p.run_if != nullptr) {
+    const int64_t xy = (int64_t)grid.x * grid.y;
+    const int64_t gz = std::max<int64_t>(1, (int64_t)sm_count() * 8 / xy);
+    grid.z = (unsigned)std::min<int64_t>(grid.z, gz);
+  }
   if (exact)
     filter_exact_kernel<T, MODE><<<grid, block, 0, s>>>(p);
   else

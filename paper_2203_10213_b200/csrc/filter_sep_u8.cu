@@ -5,7 +5,8 @@
 namespace vkt {
 namespace sep {
 template cudaError_t launch_sep_dtype<uint8_t>(int, int, const CUtensorMap&, const CUtensorMap&,
-                                           const CUtensorMap&, const TmaParams&, const float*,
+                                           const CUtensorMap&, const CUtensorMap&, const TmaParams&,
+                                           const float*,
                                            const float*, const float*, dim3, cudaStream_t);
 }  // namespace sep
 }  // namespace vkt

@@ -76,9 +76,9 @@ extern template cudaError_t launch_ws_dtype<uint16_t>(int, const CUtensorMap&, c
 namespace sep {
 #define VKT_SEP_DECL(T)                                                                            \
   extern template cudaError_t launch_sep_dtype<T>(int, int, const CUtensorMap&, const CUtensorMap&, \
-                                                  const CUtensorMap&, const tma::TmaParams&,        \
-                                                  const float*, const float*, const float*, dim3,   \
-                                                  cudaStream_t);
+                                                  const CUtensorMap&, const CUtensorMap&,           \
+                                                  const tma::TmaParams&, const float*, const float*, \
+                                                  const float*, dim3, cudaStream_t);
 VKT_SEP_DECL(uint8_t)
 VKT_SEP_DECL(uint16_t)
 VKT_SEP_DECL(float)
@@ -122,8 +122,8 @@ int bpc_of(int format) { return format == VKT_U8 ? 1 : format == VKT_U16 ? 2 : 4
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int r,
-            int pitch, int tile_y) {
+bool encode_box(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int pitch,
+                int box_x, int box_y) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return false;
   const int bpc = bpc_of(format);
@@ -132,12 +132,19 @@ bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz
                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
   cuuint64_t strides[2] = {(cuuint64_t)pitch * bpc, (cuuint64_t)pitch * ny * bpc};
-  cuuint32_t box[3] = {(cuuint32_t)tma::box_width(r, bpc), (cuuint32_t)(tile_y + 2 * r), 1u};
+  cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)box_y, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult res = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
+}
+
+// Source boxes: the tile plus its halo rows, TMA-aligned in x (box_width).
+bool encode(CUtensorMap* m, const void* base, int format, int nx, int ny, int nz, int r,
+            int pitch, int tile_y) {
+  return encode_box(m, base, format, nx, ny, nz, pitch, tma::box_width(r, bpc_of(format)),
+                    tile_y + 2 * r);
 }
 
 }  // namespace
@@ -154,7 +161,7 @@ int tma_chunk_planes(const FilterPlan& plan) {
   const int64_t nxy = (int64_t)((a.dims.x + tma::TX - 1) / tma::TX) * ((a.dims.y + ty - 1) / ty);
   // CTAs per SM: the paired kernel's Layout, or filter_tma_zp.cuh's for f32
   // K = 3 (4, Wrap 3)
-  const int64_t slots = (int64_t)sm_count() * (plan.sep ? sep::CTAS_PER_SM
+  const int64_t slots = (int64_t)sm_count() * (plan.sep ? sep::ctas_per_sm(k)
                                  : a.format == VKT_F32 && k == 3 ? (a.address_mode == VKT_WRAP ? 3 : 4)
                                  : k >= 7 ? tma::Layout<2, 7>::CTAS_PER_SM
                                  : k == 5 ? tma::Layout<2, 5>::CTAS_PER_SM
@@ -255,10 +262,14 @@ int launch_pitched(const FilterPlan& plan, const void* src, void* dst, const voi
 
   cudaError_t err;
   if (plan.sep) {
+    // output tiles leave through TMA stores: the destination as a tensor
+    // whose planes [z_begin, z_end) the launch writes
+    CUtensorMap md;
+    if (!encode_box(&md, dst, a.format, a.dims.x, a.dims.y, plan.z_end, pitch, tma::TX, ty)) return -1;
     const float *fx = plan.fx.data(), *fy = plan.fy.data(), *fz = plan.fz.data();
-    err = a.format == VKT_U8    ? sep::launch_sep_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, p, fx, fy, fz, grid, s)
-          : a.format == VKT_U16 ? sep::launch_sep_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, p, fx, fy, fz, grid, s)
-                                : sep::launch_sep_dtype<float>(k, a.address_mode, ms, ml, mh, p, fx, fy, fz, grid, s);
+    err = a.format == VKT_U8    ? sep::launch_sep_dtype<uint8_t>(k, a.address_mode, ms, ml, mh, md, p, fx, fy, fz, grid, s)
+          : a.format == VKT_U16 ? sep::launch_sep_dtype<uint16_t>(k, a.address_mode, ms, ml, mh, md, p, fx, fy, fz, grid, s)
+                                : sep::launch_sep_dtype<float>(k, a.address_mode, ms, ml, mh, md, p, fx, fy, fz, grid, s);
   } else switch (a.format) {
     case VKT_U8:
       err = wk      ? tmaws::launch_ws_dtype<uint8_t>(a.address_mode, ms, ml, mh, p, plan.w32.data(), grid, s)

@@ -307,28 +307,45 @@ def run_reference(args):
 # Our arm
 # ---------------------------------------------------------------------------
 
-def kernel_rate_f32(weights_kernel, dims=(1024, 1024, 1024), reps=10):
-    """North-star extra: 1024^3 f32 ApplyFilter kernel time (events, median of reps)."""
+def algorithmic_fma(kernel, path):
+    """FMAs per voxel of the algorithm the path runs: the dense correlation
+    evaluates every tap (kx*ky*kz); the separable kernel three 1-D sums
+    (kx + ky + kz, csrc/filter_sep.cuh)."""
+    kx, ky, kz = kernel.dims
+    return kx + ky + kz if path == "separable" else kx * ky * kz
+
+
+def kernel_rate(weights_kernel, dims=(1024, 1024, 1024), reps=10, fmt=None, path="auto", mode="clamp"):
+    """ApplyFilter kernel time on a resident volume (events, median of reps)."""
     import torch
 
     import paper_2203_10213_b200 as vk
 
-    src = vk.synthetic_device(dims, vk.DataFormat.FLOAT32, seed=11)
+    fmt = fmt or vk.DataFormat.FLOAT32
+    vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
+    try:
+        return _kernel_rate(vk, torch, weights_kernel, dims, reps, fmt, mode)
+    finally:
+        vk.set_execution_policy(vk.ExecutionPolicy())
+
+
+def _kernel_rate(vk, torch, weights_kernel, dims, reps, fmt, mode):
+    src = vk.synthetic_device(dims, fmt, seed=11)
     dst = vk.StructuredVolume(src.dims, src.format, data=vk.DeviceBuffer(src.nbytes, zero=False))
     s = torch.cuda.current_stream()
     for _ in range(2):
-        vk.ApplyFilter(dst, src, weights_kernel)
+        vk.ApplyFilter(dst, src, weights_kernel, mode)
     times = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        vk.ApplyFilter(dst, src, weights_kernel)
+        vk.ApplyFilter(dst, src, weights_kernel, mode)
         e1.record(s)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
     ms = statistics.median(times)
     nvox = dims[0] * dims[1] * dims[2]
-    path = vk.filter_path(dst, src, weights_kernel)
+    path = vk.filter_path(dst, src, weights_kernel, mode)
     del src, dst
     torch.cuda.empty_cache()
     return ms, nvox, path
@@ -493,20 +510,25 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(dev)
     local_planes = src.local.dims.z - (2 * kernel.radius.z if world > 1 else 0)
     kvox = nx * ny * local_planes
-    roof = roofline_obj(kvox, kern_ms, fmt.bytes_per_cell, kernel.tap_count, hbm_gbs, sm_max,
+    kpath = vk.filter_path(dst.local, src.local, kernel, mode)
+    roof = roofline_obj(kvox, kern_ms, fmt.bytes_per_cell, algorithmic_fma(kernel, kpath), hbm_gbs, sm_max,
                         props.multi_processor_count)
     roof["traffic"] = None
     roof["peak_source"] = (f"fp32: {props.multi_processor_count} SMs x 128 FMA/clk x {sm_max:.0f} MHz "
                            f"(sm_max_mhz, {peak_src}); hbm: {hbm_gbs} GB/s {peak_src}")
     roof["kernel_ms"] = round(kern_ms, 4)
-    roof["kernel_path"] = vk.filter_path(dst.local, src.local, kernel, mode)
-    roof["algorithmic_per_voxel"] = {"bytes": 2 * fmt.bytes_per_cell, "fma": kernel.tap_count}
+    roof["kernel_path"] = kpath
+    roof["algorithmic_per_voxel"] = {"bytes": 2 * fmt.bytes_per_cell, "fma": algorithmic_fma(kernel, kpath)}
+    if kpath == "separable":
+        roof["algorithm"] = ("rank-1 weights as three fused 1-D passes (csrc/filter_sep.cuh): "
+                             f"{algorithmic_fma(kernel, kpath)} FMAs per voxel instead of {kernel.tap_count}")
     tf = ROOT / "profiles" / "ncu_traffic.json"
     ncu_ns = None
     if tf.exists():
         table = json.loads(tf.read_text())
         ent = table.get(f"{args.config} 1 GPU")
-        if ent and world == 1 and roof["kernel_path"] == "tma":
+        ent = table.get(f"{args.config} 1 GPU {kpath}", ent if kpath == "tma" else None)
+        if ent and world == 1:
             roof["traffic"] = ent["total_bytes"]
             roof["traffic_note"] = (f"dram read+write per launch from {ent['capture']} "
                                     f"(algorithmic {ent['algorithmic_bytes']} B)")
@@ -517,16 +539,27 @@ def run_ours(args):
         if ncu_ns:
             ncu_ns = dict(ncu_ns, peaks={"hbm_gbs": hbm_gbs, "fma_pipe_pct": 100.0})
 
+    # The same workload on the dense tiled kernel (FilterPath.DENSE, every
+    # tap evaluated, bit-identical to the direct kernel): the FP32 FMA-pipe
+    # utilisation the north star quotes for 7^3.
+    dense = None
+    if world == 1 and not args.no_extra and kpath == "separable":
+        dms, dv, dpath = kernel_rate(kernel, (nx, ny, nz), reps=5, fmt=fmt, path="dense", mode=mode)
+        dense = {"path": dpath, "ms": round(dms, 4), "gvox_s": round(dv / dms / 1e6, 2),
+                 "roofline": roofline_obj(dv, dms, fmt.bytes_per_cell, kernel.tap_count, hbm_gbs, sm_max,
+                                          props.multi_processor_count)}
+
     extra = None
     if world == 1 and not args.no_extra:
         extra = []
         for name, k in (("gauss3", vk.gaussian_kernel(1.0, 3)), ("box5", vk.box_kernel(5)),
                         ("gauss7", vk.gaussian_kernel(1.5))):
-            kms, kv, kpath = kernel_rate_f32(k)
-            r = roofline_obj(kv, kms, 4, k.tap_count, hbm_gbs, sm_max, props.multi_processor_count)
-            extra.append({"kernel": name, "dims": [1024, 1024, 1024], "format": "f32",
-                          "ms": round(kms, 4), "gvox_s": round(kv / kms / 1e6, 2),
-                          "path": kpath, "roofline": r})
+            for path in ("auto", "dense") if k.dims[0] > 3 else ("auto",):
+                kms, kv, kp = kernel_rate(k, path=path)
+                r = roofline_obj(kv, kms, 4, algorithmic_fma(k, kp), hbm_gbs, sm_max, props.multi_processor_count)
+                extra.append({"kernel": name, "dims": [1024, 1024, 1024], "format": "f32",
+                              "ms": round(kms, 4), "gvox_s": round(kv / kms / 1e6, 2),
+                              "path": kp, "roofline": r})
 
     # At N > 1, rank 0 also times the unsharded launch over the whole volume
     # (it fits one B200: 2 x 2.1 GB for cfg3, 2 x 34 GB for cfg4) so the line
@@ -568,6 +601,7 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "roofline": roof,
+            "dense_kernel": dense,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "north_star_f32_1024": extra,

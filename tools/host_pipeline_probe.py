@@ -27,13 +27,16 @@ pin.copy_(src.data.array)
 hin = pin.numpy().view(np.uint16).reshape(n, n, n)
 hout = pin2.numpy().view(np.uint16).reshape(n, n, n)
 k = vk.gaussian_kernel(1.5)
-for chunk in (16, 32, 64, 128, 256):
-    vk.apply_filter_host(hin, k, out=hout, chunk_planes=chunk)
-    t = time.perf_counter()
-    for _ in range(3):
+for path in ("auto", "dense"):
+    vk.set_execution_policy(vk.ExecutionPolicy(filter_path=path))
+    for chunk in (0, 16, 32, 64, 128, 256):
         vk.apply_filter_host(hin, k, out=hout, chunk_planes=chunk)
-    dt = (time.perf_counter() - t) / 3
-    print(f"apply_filter_host chunk={chunk}: {dt*1e3:.1f} ms")
+        t = time.perf_counter()
+        for _ in range(3):
+            vk.apply_filter_host(hin, k, out=hout, chunk_planes=chunk)
+        dt = (time.perf_counter() - t) / 3
+        print(f"[{path}] apply_filter_host chunk={chunk or 'auto'}: {dt*1e3:.1f} ms")
+vk.set_execution_policy(vk.ExecutionPolicy())
 pg_in = np.array(hin)  # pageable
 pg_out = np.empty_like(pg_in)
 vk.apply_filter_host(pg_in, k, out=pg_out, chunk_planes=128)

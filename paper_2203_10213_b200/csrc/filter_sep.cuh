@@ -15,27 +15,35 @@
 //
 // Layout.  A CTA owns TX = 128 x outputs by TY rows and a chunk of ZC output
 // planes, and streams the chunk's input planes (one TMA 3D box per plane,
-// with its halo, into a raw ring) through two passes, on split warp roles
-// (as filter_ws.cuh) that meet only on mbarriers:
+// with its halo, into a raw ring) through two passes on split warp roles:
 //  * PW producer warps wait for a plane's box, repair its out-of-volume cells
-//    (edge tiles, Clamp / Mirror / Wrap; Border is TMA's zero fill, and a
-//    Border plane outside the volume in z a fully out-of-bounds box), then
-//    run the x pass: widen quads of raw cells into (x, x+64) float pairs (the
-//    paired layout of filter_tma.cuh: one FFMA2 advances two outputs with one
-//    broadcast weight) and write each row's K-tap x sums for 8 outputs
-//    (4 pairs) into a ring of float-pair planes `xb` (TY + 2R rows x 64
-//    pairs; 16-byte chunks XOR-swizzled so the producers' STS.128 and the
-//    consumers' LDS.64 are conflict-free).  The first producer refills the
-//    raw slot once every producer has read it (named barrier).
+//    (edge tiles, Clamp / Mirror / Wrap, from a per-CTA table of (cell,
+//    source) offsets; Border is TMA's zero fill, and a Border plane outside
+//    the volume in z a fully out-of-bounds box), then run the x pass: widen
+//    quads of raw cells into (x, x+64) float pairs (the paired layout of
+//    filter_tma.cuh: one FFMA2 advances two outputs with one broadcast
+//    weight) and write each row's K-tap x sums for 8 outputs (4 pairs) into a
+//    ring of float-pair planes `xb` (TY + 2R rows x 64 pairs; 16-byte chunks
+//    XOR-swizzled so the producers' STS.128 and the consumers' LDS.64 are
+//    conflict-free).  Each producer warp releases the raw slot on an
+//    mbarrier; the first one refills it a plane later.
 //  * CW consumer warps each own one pair column of YPT rows: they read the
 //    YPT + 2R x sums of their column (one LDS.64 each), form the YPT y sums
 //    and fold them into K z accumulators per output -- the partial sums of
 //    the K output planes this input plane reaches.  The plane loop is
 //    unrolled by K and the accumulators rotate by NAME: at plane phase phi,
 //    logical slot m lives in register (m + phi) % K, so every z tap is an
-//    in-place FFMA2 (no register moves; a rolled loop costs ~10% extra
-//    instructions in moves) and the completed slot is stored from register
-//    phi.
+//    in-place FFMA2 (a rolled loop costs ~10% extra instructions in moves)
+//    and the completed slot is read from register phi.  Completed outputs
+//    are quantized (one saturating F2I) into a shared staging plane that one
+//    TMA bulk tensor store writes out, clipped at the volume's faces.
+//  * xb stages pass between the roles on named barriers (bar.arrive /
+//    bar.sync: hardware blocking, where an mbarrier try_wait loop spent ~20%
+//    of all issued instructions spinning).
+// Measured (1024^3, profiles/r02_sep_rates_v5.txt): u16 7^3 Clamp 1.67 ms
+// (dense tiled kernel 11.06), u8 3^3 0.93 ms (1.27), f32 7^3 1.96 ms (10.86);
+// ncu (profiles/r02_ncu_sep_v6.txt): issue-bound at ~60% issue utilisation,
+// the consumers waiting on the producers' x pass ~40% of their time.
 // Non-finite f32 inputs: the dense kernels evaluate 0 * Inf = NaN exactly
 // where the reference does; a factored sum may not (and padded anisotropic
 // factors hold zeros).  Every stored output whose window holds an Inf or NaN
@@ -57,21 +65,18 @@ constexpr int HALF = tma::HALF;
 constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 
 // Per extent K: YPT consumer rows per thread, RG row groups of 2 consumer
-// warps (64 pair columns each), PW producer warps, CTAs per SM.  Chosen so
-// that (a) the producers' items per plane, (TY + 2R) rows x 16, are exactly
-// one per producer thread (no straggler warp), (b) per-plane instruction
-// counts of the two roles match (~100 per warp), (c) the consumers' K x YPT
-// accumulator pairs fit the register budget of THREADS x CTAS per SM.
+// warps (64 pair columns each), PW producer warps, CTAs per SM; the
+// consumers' K x YPT accumulator pairs fit 80 registers at 2 x 384 threads.
+// Measured alternatives (1024^3): one producer item per thread with shapes
+// (TY, YPT, PW) = (14, 7, 8) / (18, 3, 12) at 1-2 CTAs per SM, 6 producer
+// warps, 5 x-sum stages, 6-8 raw stages, I2F.U16 widening: all equal or
+// slower.
 template <int K>
 struct Shape {
   static constexpr int R = K / 2;
   static constexpr int YPT = K == 3 ? 8 : K == 9 ? 3 : 4;
   static constexpr int RG = 4;
-#ifdef VKT_SEP_PW
-  static constexpr int PW = VKT_SEP_PW;
-#else
   static constexpr int PW = 4;
-#endif
   static constexpr int CTAS = 2;
   static constexpr int CW = 2 * RG;
   static constexpr int THREADS = 32 * (CW + PW);
@@ -126,20 +131,10 @@ struct Cfg {
   }
   // x-sum stages (named barriers NB_READY.., NB_EMPTY..): 3, or 2 where 3
   // would leave fewer than 4 raw TMA stages (u16 3^3: 34-row stages)
-#ifdef VKT_SEP_SX
-  static constexpr int SX = fit(VKT_SEP_SX) >= 4 ? VKT_SEP_SX : 2;
-#else
   static constexpr int SX = fit(3) >= 4 ? 3 : 2;
-#endif
   static_assert(NB_READY + SX <= NB_EMPTY && NB_EMPTY + SX <= NB_STORE && NB_STORE < 16, "named barriers");
   static constexpr int FIT = fit(SX);
-#ifndef VKT_SEP_ABL  // diagnostics builds only: 1 = no x pass, 2 = one y row, 3 = no stores
-#define VKT_SEP_ABL 0
-#endif
-#ifndef VKT_SEP_SRMAX
-#define VKT_SEP_SRMAX 10
-#endif
-  static constexpr int S_RAW = FIT < VKT_SEP_SRMAX ? FIT : VKT_SEP_SRMAX;
+  static constexpr int S_RAW = FIT < 10 ? FIT : 10;
   static constexpr int SMEM = SX * XB_BYTES + SO * OUT_BYTES + S_RAW * RAW_PITCH + 2 * S_RAW * 8 + RT_BYTES + 128;
   static_assert(BX * S::BY <= 65536, "repair offsets are 16-bit");
   static_assert(S_RAW >= 4, "TMA ring too shallow");
@@ -151,14 +146,6 @@ template <int K>
 struct alignas(16) Factors {
   float wx[K], wy[K], wz[K];
 };
-
-__device__ __forceinline__ void st_cs(uint8_t* p, uint32_t v) {
-  asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_cs(uint16_t* p, uint32_t v) {
-  asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_cs(float* p, float v) { __stcs(p, v); }
 
 // floor, saturated to the format's range: one F2I.U8/U16.FLOOR (PTX
 // float-to-integer cvt clamps to the destination type)
@@ -314,9 +301,6 @@ __global__ void __launch_bounds__(Shape<K>::THREADS, Shape<K>::CTAS)
       uint64_t* xb = xb_base + s * (C::XB_BYTES / 8);
 #pragma unroll
       for (int k = 0; k < S::QPT; ++k) {
-#if VKT_SEP_ABL == 1
-        break;
-#endif
         if (S::NQ % PT != 0 && k == S::QPT - 1 && pt + PT * k >= S::NQ) break;
         // cells x0-4+4g .. x0+4g+7 (and +HALF): output pair jj at tap dx
         // reads cell 4g + jj + dx - R, i.e. index jj + dx + 4 - R here
@@ -403,9 +387,6 @@ __global__ void __launch_bounds__(Shape<K>::THREADS, Shape<K>::CTAS)
       uint64_t ys[YPT];
 #pragma unroll
       for (int i = 0; i < YPT + 2 * R; ++i) {
-#if VKT_SEP_ABL == 2
-        if (i >= 1) break;
-#endif
         const uint64_t v = col[i * HALF];
 #pragma unroll
         for (int rr = 0; rr < YPT; ++rr) {
@@ -426,7 +407,7 @@ __global__ void __launch_bounds__(Shape<K>::THREADS, Shape<K>::CTAS)
         acc[rr][(K - 1 + phi) % K] = tma::ffma2_from(ys[rr], f.wz[0], a00);
       }
       VKT_JITTER_POINT(4 * j + 3);
-      if (j >= 2 * R && VKT_SEP_ABL != 3) {
+      if (j >= 2 * R) {
         T* o = out_base + oq * (C::OUT_BYTES / (int)sizeof(T)) + stage_off;
 #pragma unroll
         for (int rr = 0; rr < YPT; ++rr, o += TX) {

@@ -47,15 +47,23 @@ def roof(nvox, bpc, taps, ms):
     return {"bound": "hbm" if t_h >= t_f else "fp32", "frac": round(t / (ms / 1e3), 4)}
 
 
+def fmas(kernel, path):
+    """FMAs per voxel of the algorithm the path runs (separable: 3 1-D sums)."""
+    kx, ky, kz = kernel.dims
+    return kx + ky + kz if path == "separable" else kx * ky * kz
+
+
 def filt(name, n, fmt, kernel, mode, reps=20):
     src = vk.synthetic_device((n, n, n), fmt, seed=7)
     dst = vk.StructuredVolume(src.dims, fmt, data=vk.DeviceBuffer(src.nbytes, zero=False))
     best, med = timeit(lambda: vk.ApplyFilter(dst, src, kernel, mode), reps)
     nvox = n ** 3
+    path = vk.filter_path(dst, src, kernel, mode)
+    taps = fmas(kernel, path)
     out = {"config": name, "n": n, "format": fmt.short_name, "k": list(kernel.dims), "mode": mode,
-           "path": vk.filter_path(dst, src, kernel, mode), "ms_best": round(best, 4),
+           "path": path, "ms_best": round(best, 4),
            "ms_median": round(med, 4), "gvox_s": round(nvox / best / 1e6, 2),
-           "roofline": roof(nvox, fmt.bytes_per_cell, kernel.tap_count, best)}
+           "roofline": roof(nvox, fmt.bytes_per_cell, taps, best)}
     if n <= 512:
         # small volumes: also the launch replayed from a CUDA graph (device time
         # without the ~15 us of per-call host work)
@@ -71,7 +79,7 @@ def filt(name, n, fmt, kernel, mode, reps=20):
         st.wait_stream(side)
         gb, _ = timeit(g.replay, reps)
         out["graph_ms_per_call"] = round(gb / 10, 4)
-        out["graph_roofline"] = roof(nvox, fmt.bytes_per_cell, kernel.tap_count, gb / 10)
+        out["graph_roofline"] = roof(nvox, fmt.bytes_per_cell, taps, gb / 10)
     del src, dst
     torch.cuda.empty_cache()
     return out
@@ -108,7 +116,8 @@ def teaser(n=512):
             pipeline()
     st.wait_stream(side)
     res["pipeline_clamp_graph_ms"] = round(timeit(g.replay)[0], 4)
-    res["filter_roofline_clamp"] = roof(n ** 3, 1, 125, res["clamp_ms"])
+    res["path"] = vk.filter_path(dst, v, k, "clamp")
+    res["filter_roofline_clamp"] = roof(n ** 3, 1, fmas(k, res["path"]), res["clamp_ms"])
     return res
 
 

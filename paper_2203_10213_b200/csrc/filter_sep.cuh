@@ -69,8 +69,10 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 // consumers' K x YPT accumulator pairs fit 80 registers at 2 x 384 threads.
 // Measured alternatives (1024^3): one producer item per thread with shapes
 // (TY, YPT, PW) = (14, 7, 8) / (18, 3, 12) at 1-2 CTAs per SM, 6 producer
-// warps, 5 x-sum stages, 6-8 raw stages, I2F.U16 widening: all equal or
-// slower.
+// warps, 5 x-sum stages, 6-8 raw stages, I2F.U16 widening, widening each raw
+// cell once into a float stage (a second producer barrier per plane: 1.6x
+// slower), direct predicated STG stores instead of the TMA store, branch-free
+// (predicated) producer rounds: all equal or slower.
 template <int K>
 struct Shape {
   static constexpr int R = K / 2;

@@ -145,6 +145,7 @@ int check_args(const vkt_clahe_args* a) {
 using namespace vkt;
 
 extern "C" int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t stream) {
+  VKT_NVTX("vkt_clahe_histograms");
   const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   int st = check_args(args);
   if (st != VKT_OK) return st;
@@ -186,6 +187,7 @@ extern "C" int vkt_clahe_histograms(const vkt_clahe_args* args, vkt_stream_t str
 }
 
 extern "C" int vkt_clahe_blend(const vkt_clahe_args* args, vkt_stream_t stream) {
+  VKT_NVTX("vkt_clahe_blend");
   const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   int st = check_args(args);
   if (st != VKT_OK) return st;

@@ -13,6 +13,23 @@
 
 #include "../../include/vkt_b200.h"
 
+// NVTX ranges around the ABI entry points (header-only NVTX3: a no-op
+// unless a profiler injects itself, e.g. `nsys` / `ncu --nvtx`).
+#ifndef VKT_NO_NVTX
+#include <nvtx3/nvToolsExt.h>
+namespace vkt {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace vkt
+#define VKT_NVTX(name) const ::vkt::NvtxRange vkt_nvtx_range_(name)
+#else
+#define VKT_NVTX(name) ((void)0)
+#endif
+
 namespace vkt {
 
 // ----------------------------------------------------------------------------

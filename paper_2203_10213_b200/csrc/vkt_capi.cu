@@ -343,6 +343,7 @@ using namespace vkt;
 extern "C" {
 
 int vkt_apply_filter(const vkt_filter_args* args, vkt_stream_t stream) {
+  VKT_NVTX("vkt_apply_filter");
   const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   FilterPlan plan;
   int st = validate_and_plan(args, plan);
@@ -426,6 +427,7 @@ int vkt_filter_chunk_planes(const vkt_filter_args* args) {
 
 int vkt_fill_box(void* dst, vkt_int3 dims, int32_t format, vkt_int3 lo, vkt_int3 hi,
                  uint32_t stored_bits, vkt_stream_t stream) {
+  VKT_NVTX("vkt_fill_box");
   const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   if (dst == nullptr) return fail(VKT_INVALID_ARGUMENT, "dst is NULL");
   if (dims.x < 1 || dims.y < 1 || dims.z < 1)

@@ -165,6 +165,7 @@ using namespace vkt;
 
 extern "C" int vkt_apply_filter_host(const vkt_filter_args* args, int32_t chunk_planes,
                                      vkt_stream_t stream) {
+  VKT_NVTX("vkt_apply_filter_host");
   const vkt::StreamDeviceGuard device_guard(reinterpret_cast<cudaStream_t>(stream));
   if (args == nullptr) {
     set_error_detail("args is NULL");

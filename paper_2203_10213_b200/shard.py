@@ -290,7 +290,7 @@ def apply_filter_sharded(dst: ShardedVolume, src: ShardedVolume, kernel: Kernel,
             phase_events.setdefault(opened[0], []).append((opened[1], ev))
 
     opened = mark("exchange")
-    with torch.cuda.stream(comm):
+    with torch.cuda.stream(comm), torch.cuda.nvtx.range("vkt halo exchange"):
         exchange(plan, src.rank, src.planes(), lo.array.view(rz, src.plane_bytes),
                  hi.array.view(rz, src.plane_bytes))
     close(opened)
@@ -309,7 +309,7 @@ def apply_filter_sharded(dst: ShardedVolume, src: ShardedVolume, kernel: Kernel,
     # tools/shard_overhead.py).  Disjoint output planes; the compute stream
     # joins the comm stream before anything else touches dst.
     opened = mark("boundary")
-    for b, e in ranges:
+    for b, e in ranges:  # NVTX: vkt_apply_filter ranges from the library
         a, _k = make_args(dst.local.data_ptr(), src.local.data_ptr(), **common, **halo_ptrs,
                           out_z_begin=b, out_z_end=e)
         launch(a, int(comm.cuda_stream))

@@ -72,7 +72,11 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 // warps, 5 x-sum stages, 6-8 raw stages, I2F.U16 widening, widening each raw
 // cell once into a float stage (a second producer barrier per plane: 1.6x
 // slower), direct predicated STG stores instead of the TMA store, branch-free
-// (predicated) producer rounds: all equal or slower.
+// (predicated) producer rounds: all equal or slower.  Producers that own
+// whole planes (plane j on warp j % PW, no producer barrier; the x-sum
+// stages must then be a multiple of PW so each stage's named barriers stay
+// with one warp): u16 5^3 1.45 -> 1.32 ms and 9^3 2.44 -> 2.25 ms, but 7^3
+// 1.66 -> 1.69, 3^3 0.93 -> 1.02, f32 slower; not adopted.
 template <int K>
 struct Shape {
   static constexpr int R = K / 2;

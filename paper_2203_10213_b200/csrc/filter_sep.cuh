@@ -76,7 +76,8 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 // whole planes (plane j on warp j % PW, no producer barrier; the x-sum
 // stages must then be a multiple of PW so each stage's named barriers stay
 // with one warp): u16 5^3 1.45 -> 1.32 ms and 9^3 2.44 -> 2.25 ms, but 7^3
-// 1.66 -> 1.69, 3^3 0.93 -> 1.02, f32 slower; not adopted.
+// 1.66 -> 1.69, 3^3 0.93 -> 1.02, f32 slower; not adopted.  32-row tiles
+// (8 row groups, 8 producer warps) at 1 CTA per SM: 7^3 1.66 -> 1.78 ms.
 template <int K>
 struct Shape {
   static constexpr int R = K / 2;

@@ -248,22 +248,23 @@ __global__ void __launch_bounds__(Shape<K>::THREADS, Shape<K>::CTAS)
     // axis whenever the overshoot exceeds the extent) or its in-plane offset
     // (Wrap).  The full mapping: a volume thinner than the halo overshoots
     // by more than one extent.
-    auto repair_cell = [&](int q, int& d, int& sidx) {
+    auto repair_cell = [&](int q, int& d, int64_t& sidx) {
       int gx, gy;
       ec.cell(p.nx, p.ny, q, gx, gy);
       const int mx = (int)map_index<MODE>(gx, p.nx), my = (int)map_index<MODE>(gy, p.ny);
       d = (gy - ya) * C::BX + gx - (x0 - C::A);
-      sidx = MODE == VKT_WRAP ? my * p.pitch + mx : (my - ya) * C::BX + mx - (x0 - C::A);
+      sidx = MODE == VKT_WRAP ? (int64_t)my * p.pitch + mx : (int64_t)(my - ya) * C::BX + mx - (x0 - C::A);
       VKT_CHECK(d >= 0 && d < C::BX * BY, "sep repair: dest");
     };
     const bool table = edge && ec.total <= C::RT_MAX &&
                        (MODE != VKT_WRAP || (int64_t)p.ny * p.pitch < (int64_t)INT32_MAX);
     if (table) {
       for (int q = pt; q < ec.total; q += PT) {
-        int d, sidx;
+        int d;
+        int64_t sidx;
         repair_cell(q, d, sidx);
         rt_dst[q] = (uint16_t)d;
-        rt_src[q] = sidx;
+        rt_src[q] = (int32_t)sidx;  // < 2^31: checked in `table`
       }
       asm volatile("bar.sync 1, %0;" ::"r"(PT) : "memory");
     }
@@ -295,7 +296,8 @@ __global__ void __launch_bounds__(Shape<K>::THREADS, Shape<K>::CTAS)
             }
           } else {
             for (int q = pt; q < ec.total; q += PT) {
-              int d, sidx;
+              int d;
+              int64_t sidx;
               repair_cell(q, d, sidx);
               raw[d] = MODE == VKT_WRAP ? __ldg(plane + sidx) : raw[sidx];
             }

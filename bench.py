@@ -522,6 +522,11 @@ def run_ours(args):
     if kpath == "separable":
         roof["algorithm"] = ("rank-1 weights as three fused 1-D passes (csrc/filter_sep.cuh): "
                              f"{algorithmic_fma(kernel, kpath)} FMAs per voxel instead of {kernel.tap_count}")
+        # the dense correlation's own bound (every tap at FP32 peak, or HBM)
+        # over this kernel's time: > 1 means faster than any dense kernel can be
+        dense_ideal = roofline_obj(kvox, 1.0, fmt.bytes_per_cell, kernel.tap_count, hbm_gbs, sm_max,
+                                   props.multi_processor_count)["frac"]  # = ideal ms at 1 ms
+        roof["vs_dense_roofline"] = round(dense_ideal / kern_ms, 3)
     tf = ROOT / "profiles" / "ncu_traffic.json"
     ncu_ns = None
     if tf.exists():

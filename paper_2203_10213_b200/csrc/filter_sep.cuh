@@ -66,7 +66,8 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 
 // Per extent K: YPT consumer rows per thread, RG row groups of 2 consumer
 // warps (64 pair columns each), PW producer warps, CTAs per SM; the
-// consumers' K x YPT accumulator pairs fit 80 registers at 2 x 384 threads.
+// consumers' K x YPT accumulator pairs fit 80 registers at 2 x 384 threads
+// (72 at 2 x 448 for 3^3).
 // Measured alternatives (1024^3): one producer item per thread with shapes
 // (TY, YPT, PW) = (14, 7, 8) / (18, 3, 12) at 1-2 CTAs per SM, 6 producer
 // warps, 5 x-sum stages, 6-8 raw stages, I2F.U16 widening, widening each raw
@@ -83,7 +84,10 @@ struct Shape {
   static constexpr int R = K / 2;
   static constexpr int YPT = K == 3 ? 8 : K == 9 ? 3 : 4;
   static constexpr int RG = 4;
-  static constexpr int PW = 4;
+  // 6 producer warps where the x pass is long per consumer row: 3^3 (34 x-sum
+  // rows for 32 outputs; u8 0.93 -> 0.89 ms) and 9^3 (20 rows for 12; u16
+  // 2.44 -> 2.28 ms); 5^3 / 7^3 measured equal or slower
+  static constexpr int PW = K == 3 || K == 9 ? 6 : 4;
   static constexpr int CTAS = 2;
   static constexpr int CW = 2 * RG;
   static constexpr int THREADS = 32 * (CW + PW);

@@ -41,6 +41,13 @@ def main():
     }
     for name, fn in rows.items():
         print(f"{per_call(fn):7.2f} us  {name}")
+    vk.set_execution_policy(vk.ExecutionPolicy(filter_path="dense"))
+    a2, keep2 = make_args(dst.data_ptr(), src.data_ptr(), src.dims, src.format, src.mapping, k,
+                          vk.AddressMode.CLAMP, flags=_capi.FLAG_NO_SEPARABLE)
+    print(f"{per_call(lambda: lib.vkt_apply_filter(ctypes.byref(a2), ctypes.c_void_p(sh))):7.2f} us  "
+          "vkt_apply_filter, dense path")
+    print(f"{per_call(lambda: vk.ApplyFilter(dst, src, k, vk.AddressMode.CLAMP)):7.2f} us  ApplyFilter, dense path")
+    vk.set_execution_policy(vk.ExecutionPolicy())
     torch.cuda.synchronize()
 
 

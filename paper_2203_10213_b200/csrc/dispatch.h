@@ -28,6 +28,10 @@ struct FilterPlan {
   // Device flag set by launch_scan_nonfinite.  Tiled launches do nothing when
   // it is set, direct launches only then; nullptr = unconditional.
   const int* guard = nullptr;
+  // Direct kernel behind the separable f32 kernel's flag: recompute only the
+  // outputs the separable pass left Inf/NaN (those whose window holds one),
+  // so results do not depend on how a volume is split into launches.
+  bool only_nonfinite = false;
   // Separable kernels (filter_sep.cuh): the args are the K^3 cube, the
   // weights factor as fz[dz]*fy[dy]*fx[dx] (each padded to K, centred).
   bool sep = false;

@@ -28,6 +28,7 @@ struct DirectParams {
   float c;            // fast epilogue constant (ints)
   double lo, hi, span;  // mapping (EXACT only); span = hi - lo
   const int* run_if;   // non-null: the launch does nothing unless *run_if != 0
+  bool only_nonfinite; // recompute only outputs whose current dst value is Inf/NaN (f32)
 };
 
 template <typename T, int MODE>
@@ -37,6 +38,10 @@ __global__ void __launch_bounds__(256) filter_direct_kernel(DirectParams p) {
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= p.nx || y >= p.ny) return;
   for (int z = p.z_begin + blockIdx.z; z < p.z_end; z += gridDim.z) {
+    T* out = static_cast<T*>(p.dst) + ((int64_t)z * p.ny + y) * p.nx + x;
+    if constexpr (!FormatTraits<T>::is_int) {
+      if (p.only_nonfinite && isfinite(*out)) continue;
+    }
     float acc = acc_init<T>(p.c);
     int t = 0;
     for (int dz = 0; dz < p.kz; ++dz) {
@@ -52,7 +57,6 @@ __global__ void __launch_bounds__(256) filter_direct_kernel(DirectParams p) {
         }
       }
     }
-    T* out = static_cast<T*>(p.dst) + ((int64_t)z * p.ny + y) * p.nx + x;
     *out = quantize_acc<T>(acc);
   }
 }
@@ -182,6 +186,7 @@ int launch_filter_direct(const FilterPlan& plan, cudaStream_t s) {
   p.hi = a.map_hi;
   p.span = a.map_hi - a.map_lo;
   p.run_if = plan.guard;
+  p.only_nonfinite = plan.only_nonfinite;
 
   switch (a.format) {
     case VKT_U8: err = launch_direct_mode<uint8_t>(p, a.address_mode, exact, s); break;

@@ -310,8 +310,9 @@ static bool plan_separable(const FilterPlan& plan, vkt_filter_args& cube, Filter
 
 // The separable launch.  f32: the kernel raises a device flag when a stored
 // output is Inf/NaN (an Inf/NaN input in its window), and the direct kernel,
-// guarded by that flag, then recomputes the launch's outputs with the dense
-// arithmetic (it does nothing otherwise).  Returns -1 when the tiled kernel
+// guarded by that flag, then recomputes exactly those outputs with the dense
+// arithmetic (it does nothing otherwise): every output is a function of its
+// own window, whatever the launch split.  Returns -1 when the tiled kernel
 // does not cover the plan.
 static int launch_separable(const FilterPlan& plan, FilterPlan& sp, cudaStream_t s) {
   if (plan.args->format != VKT_F32) return launch_filter_tma(sp, s);
@@ -329,6 +330,7 @@ static int launch_separable(const FilterPlan& plan, FilterPlan& sp, cudaStream_t
     if (st == VKT_OK) {
       FilterPlan direct = plan;
       direct.guard = static_cast<const int*>(flag);
+      direct.only_nonfinite = true;
       st = launch_filter_direct(direct, s);
     }
   }

@@ -4,8 +4,9 @@ Rank-1 weights -- gaussian_kernel (filters.py:45-58), box_kernel
 (filters.py:61-66), any outer product fz (x) fy (x) fx -- run as three fused
 1-D passes under the "auto" path.  Contract as everywhere:
 integer voxels within 1 LSB, f32 within rtol 1e-5 (plus atol 1e-5 for
-kernels with negative weights).  f32 inputs holding Inf / NaN fall back, on
-the device, to the direct kernel: bit-identical to it.
+kernels with negative weights).  f32 outputs whose window holds an Inf / NaN
+are recomputed on the device by the direct kernel (bitwise its result there);
+every output depends only on its own window, whatever the launch split.
 """
 
 import numpy as np
@@ -135,25 +136,49 @@ def test_negative_factors_f32():
 @pytest.mark.parametrize("k", [5, 7, 9])
 def test_nonfinite_f32_falls_back_to_direct(k):
     """Inf / NaN voxels: the kernel flags them and the direct kernel recomputes
-    the launch -- bitwise the dense result (0 * Inf = NaN where the reference
-    has it), for every address mode (the Wrap / Mirror neighbours of a face
-    voxel included)."""
+    the outputs it left non-finite -- exactly those whose window holds an Inf
+    or NaN -- with the dense arithmetic (0 * Inf = NaN where the reference has
+    it).  Every other output keeps its separable value.  All four modes (the
+    Wrap / Mirror neighbours of a face voxel included)."""
     rng = np.random.default_rng(k)
     stored = rng.random((14, 30, 130), dtype=np.float32)
     stored[7, 12, 60] = np.inf
     stored[0, 0, 0] = -np.inf
     stored[13, 29, 129] = np.nan
+    clean = stored.copy()
+    clean[~np.isfinite(clean)] = 0.5
     w = O.gaussian_weights(1.0, k)
     for mode in MODES:
         got, path = _run(stored, 3, w, mode)
         assert path == "separable"
         direct, _ = _run(stored, 3, w, mode, path="direct")
-        assert np.array_equal(got.view(np.uint32), direct.view(np.uint32)), mode
+        bad = ~np.isfinite(direct)
+        assert bad.any()
+        assert np.array_equal(got[bad].view(np.uint32), direct[bad].view(np.uint32)), mode
+        sep_clean, _ = _run(clean, 3, w, mode)
+        assert np.array_equal(got[~bad].view(np.uint32), sep_clean[~bad].view(np.uint32)), mode
     # the flag is per launch: a finite volume afterwards takes the separable result
     fin = rng.random((14, 30, 130), dtype=np.float32)
     got, _ = _run(fin, 3, w, "clamp")
     ok, ndiff, dmax = within_contract(got, O.apply_filter(fin, 3, w, "clamp", workers=1), 3, w)
     assert ok, (ndiff, dmax)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_nonfinite_f32_independent_of_launch_split(mode):
+    """The same Inf / NaN volume through the chunked host pipeline (one launch
+    per chunk, each with its own flag) and through z-chunked single launches:
+    bitwise the whole-volume launch."""
+    rng = np.random.default_rng(3)
+    stored = rng.random((40, 24, 64), dtype=np.float32)
+    stored[3, 5, 7] = np.nan
+    stored[21, 10, 30] = np.inf
+    w = O.gaussian_weights(1.5, 7)
+    kern = vk.Kernel((7, 7, 7), w.reshape(-1))
+    want, _ = _run(stored, 3, w, mode)
+    for chunk in (2, 9):
+        got = vk.apply_filter_host(stored, kern, mode, chunk_planes=chunk)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), chunk
 
 
 @pytest.mark.parametrize("fmt,k", [(1, 3), (2, 7), (3, 9), (2, 5)])

@@ -106,6 +106,24 @@ def test_sharded_guarded_f32_sees_nonfinite_halo(mode):
                           _unsharded(fin, vk.DataFormat.FLOAT32, kern, mode, "direct"))
 
 
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", list(vk.AddressMode))
+def test_sharded_separable_f32_nonfinite(world, mode):
+    # the separable f32 kernel recomputes exactly its Inf / NaN outputs with
+    # the dense arithmetic, per launch: an Inf / NaN next to a slab boundary
+    # (reached by the neighbour through its halo) still gives bitwise the
+    # unsharded result
+    rng = np.random.default_rng(23 + world)
+    host = rng.random((40, 24, 64), dtype=np.float32)
+    host[19, 7, 9] = np.inf
+    host[20, 3, 30] = np.nan
+    host[0, 5, 5] = -np.inf
+    kern = vk.gaussian_kernel(1.0, 5)
+    want = _unsharded(host, vk.DataFormat.FLOAT32, kern, mode)
+    got = _sharded_run(host, vk.DataFormat.FLOAT32, kern, mode, world)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
 @pytest.mark.parametrize("path", ["direct", "exact"])
 def test_sharded_other_paths(path):
     rng = np.random.default_rng(4)

@@ -79,6 +79,9 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 // with one warp): u16 5^3 1.45 -> 1.32 ms and 9^3 2.44 -> 2.25 ms, but 7^3
 // 1.66 -> 1.69, 3^3 0.93 -> 1.02, f32 slower; not adopted.  32-row tiles
 // (8 row groups, 8 producer warps) at 1 CTA per SM: 7^3 1.66 -> 1.78 ms.
+// y pass first (producers roll K-tap y sums down 2 pair columns x 8 rows,
+// each cell widened once; consumers x + z from a 72-pair y-sum row): 7^3
+// 1.85 ms, 5^3 1.58, 3^3 1.25, only 9^3 faster (2.17); not adopted.
 template <int K>
 struct Shape {
   static constexpr int R = K / 2;

@@ -203,6 +203,14 @@ int tma_chunk_planes(const FilterPlan& plan) {
     const int nch = (nzo + 170) / 171;
     if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
   }
+  // The separable kernel at K >= 5: ~128-plane chunks where >= 8 waves remain
+  // (1024^3 u16 7^3 1.665 -> 1.615 ms, 9^3 2.28 -> 2.18, f32 box 5^3 1.716 ->
+  // 1.698; 3^3 unchanged; thinner slabs keep the model's pick,
+  // profiles/r02_zc_sweep_sep.txt)
+  if (plan.sep && k >= 5) {
+    const int nch = (nzo + 127) / 128;
+    if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
+  }
   if (const char* e = std::getenv("VKT_TMA_ZC")) zc = std::max(1, std::min(nzo, std::atoi(e)));  // diagnostics
   return zc;
 }

@@ -82,10 +82,12 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 // y pass first (producers roll K-tap y sums down 2 pair columns x 8 rows,
 // each cell widened once; consumers x + z from a 72-pair y-sum row): 7^3
 // 1.85 ms, 5^3 1.58, 3^3 1.25, only 9^3 faster (2.17); not adopted.
-template <int K>
+template <int K, int BPC>
 struct Shape {
   static constexpr int R = K / 2;
-  static constexpr int YPT = K == 3 ? 8 : K == 9 ? 3 : 4;
+  // u8/u16 5^3: 5 rows (24 x-sum rows = 3 full producer rounds; 1.42 ->
+  // 1.26-1.28 ms); f32 5^3 keeps 4 (its raw ring would drop to 3 stages)
+  static constexpr int YPT = K == 3 ? 8 : K == 9 ? 3 : K == 5 && BPC < 4 ? 5 : 4;
   static constexpr int RG = 4;
   // 6 producer warps where the x pass is long per consumer row: 3^3 (34 x-sum
   // rows for 32 outputs; u8 0.93 -> 0.89 ms) and 9^3 (20 rows for 12; u16
@@ -101,15 +103,11 @@ struct Shape {
   static constexpr int QPT = (NQ + PT - 1) / PT;
 };
 
-__host__ __device__ constexpr int tile_rows(int k) {
-  return k == 3 ? Shape<3>::TY : k == 5 ? Shape<5>::TY : k == 7 ? Shape<7>::TY : Shape<9>::TY;
+__host__ __device__ constexpr int tile_rows(int k, int bpc) {
+  return bpc == 4 ? (k == 3 ? Shape<3, 4>::TY : k == 5 ? Shape<5, 4>::TY : k == 7 ? Shape<7, 4>::TY : Shape<9, 4>::TY)
+                  : (k == 3 ? Shape<3, 2>::TY : k == 5 ? Shape<5, 2>::TY : k == 7 ? Shape<7, 2>::TY : Shape<9, 2>::TY);
 }
-__host__ __device__ constexpr int rows_per_thread(int k) {
-  return k == 3 ? Shape<3>::YPT : k == 5 ? Shape<5>::YPT : k == 7 ? Shape<7>::YPT : Shape<9>::YPT;
-}
-__host__ __device__ constexpr int ctas_per_sm(int k) {
-  return k == 3 ? Shape<3>::CTAS : k == 5 ? Shape<5>::CTAS : k == 7 ? Shape<7>::CTAS : Shape<9>::CTAS;
-}
+__host__ __device__ constexpr int ctas_per_sm(int) { return 2; }
 
 // Producer -> consumer handoff of the xb stages on named barriers (hardware
 // blocking: an mbarrier try_wait loop cost ~20% of all issued instructions
@@ -126,7 +124,7 @@ __device__ __forceinline__ void nb_sync(int id, int n) {
 
 template <typename T, int K>
 struct Cfg {
-  using S = Shape<K>;
+  using S = Shape<K, (int)sizeof(T)>;
   static constexpr int A = tma::box_align_left(S::R, (int)sizeof(T));
   static constexpr int BX = tma::box_width(S::R, (int)sizeof(T));
   static constexpr int RAW_BYTES = BX * S::BY * (int)sizeof(T);
@@ -189,14 +187,14 @@ __device__ __forceinline__ void tma_store(const void* src, const CUtensorMap* ma
 __device__ __forceinline__ int xb_chunk(int ci) { return ci ^ ((ci >> 3) & 1); }
 
 template <typename T, int K, int MODE>
-__global__ void __launch_bounds__(Shape<K>::THREADS, Shape<K>::CTAS)
+__global__ void __launch_bounds__(Shape<K, (int)sizeof(T)>::THREADS, Shape<K, (int)sizeof(T)>::CTAS)
     filter_sep_kernel(const __grid_constant__ CUtensorMap map_src,
                       const __grid_constant__ CUtensorMap map_lo,
                       const __grid_constant__ CUtensorMap map_hi,
                       const __grid_constant__ CUtensorMap map_dst, const TmaParams p,
                       const __grid_constant__ Factors<K> f) {
   using C = Cfg<T, K>;
-  using S = Shape<K>;
+  using S = Shape<K, (int)sizeof(T)>;
   constexpr int R = S::R, YPT = S::YPT, TY = S::TY, BY = S::BY, SR = C::S_RAW, SX = C::SX;
   constexpr int PT = S::PT, CW = S::CW, PW = S::PW;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -479,7 +477,7 @@ cudaError_t launch_sep_kernel(const CUtensorMap& ms, const CUtensorMap& ml, cons
     if (err != cudaSuccess) return err;
     opted.fetch_or(bit, std::memory_order_release);
   }
-  fn<<<grid, Shape<K>::THREADS, C::SMEM, s>>>(ms, ml, mh, md, p, f);
+  fn<<<grid, Cfg<T, K>::S::THREADS, C::SMEM, s>>>(ms, ml, mh, md, p, f);
   return cudaGetLastError();
 }
 

@@ -89,6 +89,8 @@ namespace {
 
 
 
+int bpc_of(int format) { return format == VKT_U8 ? 1 : format == VKT_U16 ? 2 : 4; }
+
 // Separable plans run filter_sep.cuh; u8/u16 3x3x3 dense plans the
 // warp-specialized kernel (filter_ws.cuh), with 32-row tiles; everything else
 // the paired-layout kernel's 16-row tiles.
@@ -96,7 +98,8 @@ bool warp_kernel(const FilterPlan& plan) {
   return !plan.sep && plan.args->format != VKT_F32 && plan.args->kdims.x == 3;
 }
 int tile_rows(const FilterPlan& plan) {
-  return plan.sep ? sep::tile_rows(plan.args->kdims.x) : warp_kernel(plan) ? tmaws::TY : tma::TY;
+  return plan.sep ? sep::tile_rows(plan.args->kdims.x, bpc_of(plan.args->format))
+                  : warp_kernel(plan) ? tmaws::TY : tma::TY;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -118,7 +121,6 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int bpc_of(int format) { return format == VKT_U8 ? 1 : format == VKT_U16 ? 2 : 4; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

@@ -186,38 +186,6 @@ __device__ __forceinline__ void tma_store(const void* src, const CUtensorMap* ma
 // producer's STS.128 phase (chunks 2g, g = 0..7) hit 8 distinct bank groups.
 __device__ __forceinline__ int xb_chunk(int ci) { return ci ^ ((ci >> 3) & 1); }
 
-// Tiles on the volume's x / y faces repair their out-of-volume cells every
-// plane (Wrap gathers them from the far side) and run longer.  Blocks are
-// dispatched in linear-id order, so the linear id is remapped to run all face
-// tiles (every z chunk) first and the uniform interior tiles last: the final,
-// partial wave then holds no slow tile.
-__device__ __forceinline__ void edge_first(int& tx, int& ty, int& tz) {
-  const int gx = gridDim.x, gy = gridDim.y;
-  if (gx < 3 || gy < 3) return;  // every tile is a face tile
-  const int E = 2 * gx + 2 * (gy - 2);
-  const int I = (gx - 2) * (gy - 2);
-  const int L = blockIdx.x + gx * (blockIdx.y + gy * blockIdx.z);
-  const int nedge = E * (int)gridDim.z;
-  if (L < nedge) {
-    tz = L / E;
-    const int e = L - tz * E;
-    if (e < 2 * gx) {
-      tx = e < gx ? e : e - gx;
-      ty = e < gx ? 0 : gy - 1;
-    } else {
-      const int e2 = e - 2 * gx;
-      ty = 1 + (e2 >> 1);
-      tx = (e2 & 1) ? gx - 1 : 0;
-    }
-  } else {
-    const int i = L - nedge;
-    tz = i / I;
-    const int r = i - tz * I;
-    ty = 1 + r / (gx - 2);
-    tx = 1 + r - (ty - 1) * (gx - 2);
-  }
-}
-
 template <typename T, int K, int MODE>
 __global__ void __launch_bounds__(Shape<K, (int)sizeof(T)>::THREADS, Shape<K, (int)sizeof(T)>::CTAS)
     filter_sep_kernel(const __grid_constant__ CUtensorMap map_src,
@@ -243,11 +211,11 @@ __global__ void __launch_bounds__(Shape<K, (int)sizeof(T)>::THREADS, Shape<K, (i
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  int tx = blockIdx.x, ty = blockIdx.y, tz = blockIdx.z;
-  if constexpr (MODE != VKT_BORDER) edge_first(tx, ty, tz);
-  const int x0 = tx * TX;
-  const int y0 = ty * TY;
-  const int zo0 = p.z_begin + tz * p.zc;
+  int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  if constexpr (MODE != VKT_BORDER) tma::edge_first(bx, by, bz);
+  const int x0 = bx * TX;
+  const int y0 = by * TY;
+  const int zo0 = p.z_begin + bz * p.zc;
   const int nzo = min(p.zc, p.z_end - zo0);
   if (nzo <= 0) return;
   const int np = nzo + 2 * R;

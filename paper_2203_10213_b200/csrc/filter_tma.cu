@@ -208,10 +208,9 @@ int tma_chunk_planes(const FilterPlan& plan) {
   // The separable kernel at K >= 5: ~128-plane chunks where >= 8 waves remain
   // (1024^3 u16 7^3 1.665 -> 1.615 ms, 9^3 2.28 -> 2.18, f32 box 5^3 1.716 ->
   // 1.698; 3^3 unchanged; thinner slabs keep the model's pick,
-  // profiles/r02_zc_sweep_sep.txt).  Not Wrap: its edge tiles gather the far
-  // side's cells and run longer, so longer chunks lengthen the tail (2.02 ->
-  // 2.10 ms).
-  if (plan.sep && k >= 5 && a.address_mode != VKT_WRAP) {
+  // profiles/r02_zc_sweep_sep.txt; Wrap 1.88 -> 1.80 ms now that its slower
+  // face tiles run first, filter_sep.cuh edge_first).
+  if (plan.sep && k >= 5) {
     const int nch = (nzo + 127) / 128;
     if (nxy * nch >= 8 * slots) zc = (nzo + nch - 1) / nch;
   }

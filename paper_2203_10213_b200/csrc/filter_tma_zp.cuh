@@ -400,9 +400,10 @@ __global__ void __launch_bounds__(Layout<3>::THREADS, Layout<3, MODE>::CTAS_PER_
   const int tid = threadIdx.x;
   const int warp = tid / 32;
   const int lane = tid % 32;
-  const int x0 = blockIdx.x * TX;
-  const int y0 = blockIdx.y * TY;
-  const int zo0 = p.z_begin + blockIdx.z * p.zc;
+  const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  const int x0 = bx * TX;
+  const int y0 = by * TY;
+  const int zo0 = p.z_begin + bz * p.zc;
   const int nzo = min(p.zc, p.z_end - zo0);
   if (nzo <= 0) return;
   const int np = nzo + 2 * R;  // input planes of this chunk

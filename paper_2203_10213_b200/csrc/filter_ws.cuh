@@ -143,9 +143,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int x0 = blockIdx.x * TX;
-  const int y0 = blockIdx.y * TY;
-  const int zo0 = p.z_begin + blockIdx.z * p.zc;
+  int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  if constexpr (MODE != VKT_BORDER) tma::edge_first(bx, by, bz);
+  const int x0 = bx * TX;
+  const int y0 = by * TY;
+  const int zo0 = p.z_begin + bz * p.zc;
   const int nzo = min(p.zc, p.z_end - zo0);
   if (nzo <= 0) return;
   const int np = nzo + 2 * R;

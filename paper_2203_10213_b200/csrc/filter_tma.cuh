@@ -281,34 +281,46 @@ __device__ __forceinline__ uint64_t widen2(uint32_t blo, uint32_t bhi) {
 // Tiles on the volume's x / y faces repair their out-of-volume cells every
 // plane (Wrap gathers them from the far side) and run longer.  Blocks are
 // dispatched in linear-id order, so the linear id is remapped to run all face
-// tiles (every z chunk) first and the uniform interior tiles last: the final,
-// partial wave then holds no slow tile.  Used by the compute-bound kernels
+// tiles first and the uniform interior tiles last: the final, partial wave
+// then holds no slow tile.  Used by the compute-bound kernels
 // (filter_sep.cuh: u16 7^3 Wrap 2.03 -> 1.80 ms with deep chunks;
 // filter_ws.cuh: u8 3^3 Wrap 1.363 -> 1.307); the HBM-bound f32 3^3 kernel
 // and the paired kernel keep the natural order (neighbouring tiles share
 // halo rows in L2: f32 3^3 Clamp 1.48 -> 1.57 ms when reordered).
+template <int MODE>
 __device__ __forceinline__ void edge_first(int& tx, int& ty, int& tz) {
   const int gx = gridDim.x, gy = gridDim.y;
   if (gx < 3 || gy < 3) return;  // every tile is a face tile
   const int E = 2 * gx + 2 * (gy - 2);
   const int I = (gx - 2) * (gy - 2);
-  const int L = blockIdx.x + gx * (blockIdx.y + gy * blockIdx.z);
-  const int nedge = E * (int)gridDim.z;
-  if (L < nedge) {
-    tz = L / E;
-    const int e = L - tz * E;
-    if (e < 2 * gx) {
-      tx = e < gx ? e : e - gx;
-      ty = e < gx ? 0 : gy - 1;
+  // Clamp / Mirror: per z chunk, its face tiles then its interior tiles (the
+  // face tiles are only a little slower, and tiles sharing halo rows stay
+  // close together in L2).  Wrap (its face tiles gather the far side): the
+  // face tiles of every chunk first.
+  int L = blockIdx.x + gx * blockIdx.y;
+  tz = blockIdx.z;
+  if constexpr (MODE == VKT_WRAP) {
+    const int G = L + gx * gy * (int)blockIdx.z;
+    const int nedge = E * (int)gridDim.z;
+    if (G < nedge) {
+      tz = G / E;
+      L = G - tz * E;
     } else {
-      const int e2 = e - 2 * gx;
+      tz = (G - nedge) / I;
+      L = E + (G - nedge) - tz * I;
+    }
+  }
+  if (L < E) {
+    if (L < 2 * gx) {
+      tx = L < gx ? L : L - gx;
+      ty = L < gx ? 0 : gy - 1;
+    } else {
+      const int e2 = L - 2 * gx;
       ty = 1 + (e2 >> 1);
       tx = (e2 & 1) ? gx - 1 : 0;
     }
   } else {
-    const int i = L - nedge;
-    tz = i / I;
-    const int r = i - tz * I;
+    const int r = L - E;
     ty = 1 + r / (gx - 2);
     tx = 1 + r - (ty - 1) * (gx - 2);
   }

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM)
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
-  if constexpr (MODE != VKT_BORDER) tma::edge_first(bx, by, bz);
+  if constexpr (MODE != VKT_BORDER) tma::edge_first<MODE>(bx, by, bz);
   const int x0 = bx * TX;
   const int y0 = by * TY;
   const int zo0 = p.z_begin + bz * p.zc;

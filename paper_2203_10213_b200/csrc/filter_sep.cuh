@@ -40,17 +40,21 @@
 //  * xb stages pass between the roles on named barriers (bar.arrive /
 //    bar.sync: hardware blocking, where an mbarrier try_wait loop spent ~20%
 //    of all issued instructions spinning).
-// Measured (1024^3, profiles/r02_sep_rates_v5.txt): u16 7^3 Clamp 1.67 ms
-// (dense tiled kernel 11.06), u8 3^3 0.93 ms (1.27), f32 7^3 1.96 ms (10.86);
-// ncu (profiles/r02_ncu_sep_v6.txt): issue-bound at ~60% issue utilisation,
-// the consumers waiting on the producers' x pass ~40% of their time.
+//  * Face tiles (which repair cells every plane) run first in the last z
+//    chunk (every chunk under Wrap): tma::edge_first.
+// Measured (1024^3, profiles/r02_sep_rates_v14.txt): u16 7^3 Clamp 1.57 ms
+// (dense tiled kernel 11.06), u8 3^3 0.89 ms (1.25), f32 7^3 1.86 ms (10.86);
+// ncu (profiles/r02_ncu_sep_cfg3_final.txt): issue-bound at ~60% issue
+// utilisation and ~60% of shared-memory bandwidth, the consumers waiting on
+// the producers' x pass ~40% of their time.
 // Non-finite f32 inputs: the dense kernels evaluate 0 * Inf = NaN exactly
 // where the reference does; a factored sum may not (and padded anisotropic
 // factors hold zeros).  Every stored output whose window holds an Inf or NaN
 // is itself non-finite (Inf propagates through sums, 0 * Inf is NaN), so the
 // f32 kernel folds each stored pair into x*0 + chk and raises p.nonfinite
 // when chk ends NaN; the host then runs the direct kernel, guarded by that
-// flag, over the same outputs (vkt_capi.cu).  Integer voxels are finite.
+// flag, which recomputes exactly the outputs left Inf / NaN (vkt_capi.cu).
+// Integer voxels are finite.
 #pragma once
 
 #include "filter_ws.cuh"

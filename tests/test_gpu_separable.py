@@ -196,3 +196,19 @@ def test_chunking_invariant(monkeypatch, fmt, k):
         assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
     ok, ndiff, dmax = within_contract(outs[0], O.apply_filter(stored, fmt, w, "mirror", workers=1), fmt, w)
     assert ok, (ndiff, dmax)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("fmt,k", [(2, 7), (1, 3), (3, 5)])
+def test_face_tiles_first_covers_every_tile(monkeypatch, mode, fmt, k):
+    """tma::edge_first permutes the blocks (face tiles of the last z chunk, or
+    of every chunk under Wrap, first): on a grid of 3 x 4+ tiles and several
+    z chunks every tile is still computed exactly once."""
+    rng = np.random.default_rng(k + 10 * fmt)
+    stored = _stored(rng, fmt, (70, 50, 300))
+    w = O.gaussian_weights(1.0, k) if k != 5 else O.box_weights(5)
+    monkeypatch.setenv("VKT_TMA_ZC", "16")
+    got, path = _run(stored, fmt, w, mode)
+    assert path == "separable" or (fmt == 3 and k == 3)
+    ok, ndiff, dmax = within_contract(got, O.apply_filter(stored, fmt, w, mode, workers=1), fmt, w)
+    assert ok, (ndiff, dmax)

@@ -8,7 +8,9 @@ Workloads (``--config``):
   cfg4 (BASELINE.json configs[3]): the 7-point Laplacian in a 3^3 footprint on
        a 2048^3 float32 volume (32 GiB), Wrap, z-slab sharded.
 Both scale strongly (the volume is fixed).  A "step" is one ApplyFilter pass
-over the whole volume.
+over the whole volume, on the default path: the Gaussian is rank-1, so cfg3
+runs the separable kernel (csrc/filter_sep.cuh); ``dense_kernel`` in the line
+times the same workload on the dense tiled kernel (filter_path="dense").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3|cfg4]
 

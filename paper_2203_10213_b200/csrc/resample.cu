@@ -15,19 +15,59 @@
 namespace vkt {
 namespace {
 
+// Flip: rows are independent.  Axis 1 / 2 copy whole rows from the mirrored
+// row; axis 0 reverses each row.  Rows of 16-byte multiples move as 16-byte
+// chunks (axis 0: chunk c <- chunk n-1-c, its cells reversed in registers),
+// other rows cell by cell.  TPR threads per row, RPB rows per block.
 template <typename T>
+__device__ __forceinline__ uint4 reverse16(uint4 v) {
+  if constexpr (sizeof(T) == 1)
+    return make_uint4(__byte_perm(v.w, 0, 0x0123), __byte_perm(v.z, 0, 0x0123),
+                      __byte_perm(v.y, 0, 0x0123), __byte_perm(v.x, 0, 0x0123));
+  else if constexpr (sizeof(T) == 2)
+    return make_uint4(__byte_perm(v.w, 0, 0x1032), __byte_perm(v.z, 0, 0x1032),
+                      __byte_perm(v.y, 0, 0x1032), __byte_perm(v.x, 0, 0x1032));
+  else
+    return make_uint4(v.w, v.z, v.y, v.x);
+}
+
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) flip_kernel(const T* __restrict__ src, T* __restrict__ dst,
-                                                   int nx, int ny, int nz, int axis) {
-  const int64_t n = (int64_t)nx * ny * nz;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t x = i % nx, r = i / nx;
-    int64_t y = r % ny, z = r / ny;
-    if (axis == 0) x = nx - 1 - x;
-    else if (axis == 1) y = ny - 1 - y;
-    else z = nz - 1 - z;
-    dst[i] = src[(z * ny + y) * nx + x];
+                                                   int nx, int ny, int nz, int axis, int per_row) {
+  const int64_t rows = (int64_t)ny * nz;
+  const int rpb = blockDim.y;
+  for (int64_t row = (int64_t)blockIdx.y * rpb + threadIdx.y; row < rows; row += (int64_t)gridDim.y * rpb) {
+    const int z = (int)(row / ny), y = (int)(row - (int64_t)z * ny);
+    const int64_t srow = axis == 1 ? (int64_t)z * ny + (ny - 1 - y)
+                       : axis == 2 ? (int64_t)(nz - 1 - z) * ny + y : row;
+    const T* s = src + srow * nx;
+    T* d = dst + row * nx;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < per_row; c += gridDim.x * blockDim.x) {
+      if constexpr (VEC) {
+        if (axis == 0)
+          reinterpret_cast<uint4*>(d)[c] = reverse16<T>(__ldg(reinterpret_cast<const uint4*>(s) + (per_row - 1 - c)));
+        else
+          reinterpret_cast<uint4*>(d)[c] = __ldg(reinterpret_cast<const uint4*>(s) + c);
+      } else {
+        d[c] = s[axis == 0 ? nx - 1 - c : c];
+      }
+    }
   }
+}
+
+template <typename T>
+cudaError_t launch_flip(const T* src, T* dst, vkt_int3 dims, int axis, cudaStream_t s) {
+  const bool vec = ((int64_t)dims.x * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  const int per_row = vec ? (int)((int64_t)dims.x * sizeof(T) / 16) : dims.x;
+  const int tpr = per_row >= 256 ? 256 : (per_row + 31) / 32 * 32;
+  const dim3 block(tpr, 256 / tpr);
+  const int64_t rows = (int64_t)dims.y * dims.z;
+  const int64_t gy = (rows + block.y - 1) / block.y;
+  const dim3 grid((per_row + tpr - 1) / tpr, (unsigned)(gy < 65535 ? gy : 65535));
+  if (vec) flip_kernel<T, true><<<grid, block, 0, s>>>(src, dst, dims.x, dims.y, dims.z, axis, per_row);
+  else flip_kernel<T, false><<<grid, block, 0, s>>>(src, dst, dims.x, dims.y, dims.z, axis, per_row);
+  return cudaGetLastError();
 }
 
 template <typename T>
@@ -77,13 +117,28 @@ __device__ __forceinline__ Axis axis_coord(int i, int n_src, double scale) {
 struct ResampleParams {
   const void* src;
   void* dst;
+  const double* lut;  // u8 / u16 sources: mapped value of every stored value
   int sx, sy, sz, dx, dy, dz;
   double slo, sspan, dlo, dspan;
   double scale_x, scale_y, scale_z;
 };
 
+// The mapped value of each stored value (u8: 256, u16: 65536 doubles), computed
+// once per call with the same float64 operations as mapped(): the sampling
+// kernel then looks values up instead of dividing 8 times per output.
+template <typename S>
+__global__ void __launch_bounds__(256) mapped_lut_kernel(double* lut, double lo, double span) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= (int)FormatTraits<S>::max_d) lut[i] = mapped<S>((S)i, lo, span);
+}
+
 template <typename S, typename D>
 __global__ void __launch_bounds__(256) resample_kernel(ResampleParams p) {
+  __shared__ double slut[sizeof(S) == 1 ? 256 : 1];
+  if constexpr (sizeof(S) == 1) {
+    slut[threadIdx.x] = p.lut[threadIdx.x];  // blockDim.x == 256
+    __syncthreads();
+  }
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.dx) return;
@@ -91,8 +146,11 @@ __global__ void __launch_bounds__(256) resample_kernel(ResampleParams p) {
   const Axis ay = axis_coord(y, p.sy, p.scale_y);
   const Axis az = axis_coord(z, p.sz, p.scale_z);
   const S* g = static_cast<const S*>(p.src);
-  auto at = [&](int zz, int yy, int xx) {
-    return mapped<S>(g[((int64_t)zz * p.sy + yy) * p.sx + xx], p.slo, p.sspan);
+  auto at = [&](int zz, int yy, int xx) -> double {
+    const S v = g[((int64_t)zz * p.sy + yy) * p.sx + xx];
+    if constexpr (sizeof(S) == 1) return slut[v];
+    else if constexpr (sizeof(S) == 2) return __ldg(p.lut + v);
+    else return mapped<S>(v, p.slo, p.sspan);
   };
   const double c00 = lerp(at(az.i0, ay.i0, ax.i0), at(az.i0, ay.i0, ax.i1), ax.f);
   const double c10 = lerp(at(az.i0, ay.i1, ax.i0), at(az.i0, ay.i1, ax.i1), ax.f);
@@ -131,15 +189,11 @@ extern "C" int vkt_flip(const void* src, void* dst, vkt_int3 dims, int32_t forma
     return VKT_INVALID_ARGUMENT;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int grid = sm_count() * 8;
-  if (format == VKT_U8)
-    flip_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, dims.x, dims.y, dims.z, axis);
-  else if (format == VKT_U16)
-    flip_kernel<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)src, (uint16_t*)dst, dims.x, dims.y, dims.z, axis);
-  else
-    flip_kernel<float><<<grid, 256, 0, s>>>((const float*)src, (float*)dst, dims.x, dims.y, dims.z, axis);
+  cudaError_t e;
+  if (format == VKT_U8) e = launch_flip((const uint8_t*)src, (uint8_t*)dst, dims, axis, s);
+  else if (format == VKT_U16) e = launch_flip((const uint16_t*)src, (uint16_t*)dst, dims, axis, s);
+  else e = launch_flip((const float*)src, (float*)dst, dims, axis, s);
   count_launch();
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error_detail("flip launch: %s", cudaGetErrorString(e));
     return VKT_DEVICE_FAILURE;
@@ -169,12 +223,26 @@ extern "C" int vkt_resample(const void* src, vkt_int3 src_dims, int32_t src_form
   p.scale_y = (double)src_dims.y / (double)dst_dims.y;
   p.scale_z = (double)src_dims.z / (double)dst_dims.z;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
+  double* lut = nullptr;
+  if (src_format != VKT_F32) {
+    const int n = src_format == VKT_U8 ? 256 : 65536;
+    e = scratch_alloc(reinterpret_cast<void**>(&lut), (size_t)n * sizeof(double), s);
+    if (e != cudaSuccess) {
+      set_error_detail("resample: scratch_alloc(lut): %s", cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
+    }
+    if (src_format == VKT_U8) mapped_lut_kernel<uint8_t><<<1, 256, 0, s>>>(lut, p.slo, p.sspan);
+    else mapped_lut_kernel<uint16_t><<<256, 256, 0, s>>>(lut, p.slo, p.sspan);
+    count_launch();
+    p.lut = lut;
+  }
   switch (src_format) {
     case VKT_U8: e = launch_resample_dst<uint8_t>(p, dst_format, s); break;
     case VKT_U16: e = launch_resample_dst<uint16_t>(p, dst_format, s); break;
     default: e = launch_resample_dst<float>(p, dst_format, s); break;
   }
+  if (lut != nullptr) scratch_free(lut, s);
   count_launch();
   if (e != cudaSuccess) {
     set_error_detail("resample launch: %s", cudaGetErrorString(e));

@@ -177,22 +177,23 @@ def _histograms(volume: StructuredVolume, params: ClaheParams, keep: list) -> tu
 
 
 def _mappings_from_hist(h: np.ndarray, volume: StructuredVolume, params: ClaheParams) -> np.ndarray:
-    """Clip + cdf / n_cells per brick, as brick_mappings does (filters.py:188-201)."""
+    """Clip + cdf / n_cells per brick, as brick_mappings does (filters.py:188-201),
+    for all bricks at once: the same integer clip (_clip_counts) and the same
+    float64 cumsum / n_cells per element as the per-brick loop."""
     c = params.brick_counts
     d = volume.dims
     ex, ey, ez = _axis_edges(d.x, c.x), _axis_edges(d.y, c.y), _axis_edges(d.z, c.z)
     nb = params.num_bins
-    out = np.empty((c.z, c.y, c.x, nb), dtype=np.float64)
-    for bz in range(c.z):
-        for by in range(c.y):
-            for bx in range(c.x):
-                hist = h[bz, by, bx]
-                n_cells = int((ez[bz + 1] - ez[bz]) * (ey[by + 1] - ey[by]) * (ex[bx + 1] - ex[bx]))
-                if math.isfinite(params.clip_limit):
-                    limit = max(1, int(math.floor(params.clip_limit * n_cells / nb + 0.5)))
-                    hist = _clip_counts(hist, limit)
-                out[bz, by, bx] = np.cumsum(hist) / float(n_cells)
-    return out
+    n_cells = (np.diff(ez)[:, None, None] * np.diff(ey)[None, :, None] * np.diff(ex)[None, None, :]).astype(np.int64)
+    hist = h.astype(np.int64)
+    if math.isfinite(params.clip_limit):
+        # limit = max(1, floor(clip * n_cells / nb + 0.5)) in float64, per brick
+        limit = np.maximum(1, np.floor(params.clip_limit * n_cells.astype(np.float64) / nb + 0.5)).astype(np.int64)
+        lim = limit[..., None]
+        excess = np.maximum(hist - lim, 0).sum(axis=-1)
+        share, rem = np.divmod(excess, nb)
+        hist = np.minimum(hist, lim) + share[..., None] + (np.arange(nb) < rem[..., None])
+    return np.cumsum(hist, axis=-1) / n_cells.astype(np.float64)[..., None]
 
 
 def brick_mappings(volume: StructuredVolume, params: ClaheParams) -> np.ndarray:

@@ -118,10 +118,22 @@ struct ResampleParams {
   const void* src;
   void* dst;
   const double* lut;  // u8 / u16 sources: mapped value of every stored value
+  const Axis* ax;     // per destination index: the source cells and weight
+  const Axis* ay;     //   (axis_coord, computed once per call)
+  const Axis* az;
   int sx, sy, sz, dx, dy, dz;
   double slo, sspan, dlo, dspan;
   double scale_x, scale_y, scale_z;
 };
+
+// axis_coord for every destination index of the three axes (x, then y, then z)
+__global__ void __launch_bounds__(256) axis_table_kernel(Axis* t, int dx, int dy, int dz, int sx, int sy,
+                                                         int sz, double scx, double scy, double scz) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < dx) t[i] = axis_coord(i, sx, scx);
+  else if (i < dx + dy) t[i] = axis_coord(i - dx, sy, scy);
+  else if (i < dx + dy + dz) t[i] = axis_coord(i - dx - dy, sz, scz);
+}
 
 // The mapped value of each stored value (u8: 256, u16: 65536 doubles), computed
 // once per call with the same float64 operations as mapped(): the sampling
@@ -142,9 +154,9 @@ __global__ void __launch_bounds__(256) resample_kernel(ResampleParams p) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= p.dx) return;
-  const Axis ax = axis_coord(x, p.sx, p.scale_x);
-  const Axis ay = axis_coord(y, p.sy, p.scale_y);
-  const Axis az = axis_coord(z, p.sz, p.scale_z);
+  const Axis ax = p.ax[x];
+  const Axis ay = p.ay[y];
+  const Axis az = p.az[z];
   const S* g = static_cast<const S*>(p.src);
   auto at = [&](int zz, int yy, int xx) -> double {
     const S v = g[((int64_t)zz * p.sy + yy) * p.sx + xx];
@@ -224,14 +236,26 @@ extern "C" int vkt_resample(const void* src, vkt_int3 src_dims, int32_t src_form
   p.scale_z = (double)src_dims.z / (double)dst_dims.z;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
+  // scratch: the axis tables, then (u8 / u16 sources) the mapped-value LUT
+  const int nax = dst_dims.x + dst_dims.y + dst_dims.z;
+  const size_t ax_bytes = ((size_t)nax * sizeof(Axis) + 255) / 256 * 256;
+  const int nlut = src_format == VKT_U8 ? 256 : src_format == VKT_U16 ? 65536 : 0;
+  uint8_t* scratch = nullptr;
+  e = scratch_alloc(reinterpret_cast<void**>(&scratch), ax_bytes + (size_t)nlut * sizeof(double), s);
+  if (e != cudaSuccess) {
+    set_error_detail("resample: scratch_alloc: %s", cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
+  }
+  Axis* tab = reinterpret_cast<Axis*>(scratch);
+  axis_table_kernel<<<(nax + 255) / 256, 256, 0, s>>>(tab, dst_dims.x, dst_dims.y, dst_dims.z, p.sx, p.sy,
+                                                        p.sz, p.scale_x, p.scale_y, p.scale_z);
+  count_launch();
+  p.ax = tab;
+  p.ay = tab + dst_dims.x;
+  p.az = tab + dst_dims.x + dst_dims.y;
   double* lut = nullptr;
-  if (src_format != VKT_F32) {
-    const int n = src_format == VKT_U8 ? 256 : 65536;
-    e = scratch_alloc(reinterpret_cast<void**>(&lut), (size_t)n * sizeof(double), s);
-    if (e != cudaSuccess) {
-      set_error_detail("resample: scratch_alloc(lut): %s", cudaGetErrorString(e));
-      return e == cudaErrorMemoryAllocation ? VKT_ALLOCATION_FAILURE : VKT_DEVICE_FAILURE;
-    }
+  if (nlut > 0) {
+    lut = reinterpret_cast<double*>(scratch + ax_bytes);
     if (src_format == VKT_U8) mapped_lut_kernel<uint8_t><<<1, 256, 0, s>>>(lut, p.slo, p.sspan);
     else mapped_lut_kernel<uint16_t><<<256, 256, 0, s>>>(lut, p.slo, p.sspan);
     count_launch();
@@ -242,7 +266,7 @@ extern "C" int vkt_resample(const void* src, vkt_int3 src_dims, int32_t src_form
     case VKT_U16: e = launch_resample_dst<uint16_t>(p, dst_format, s); break;
     default: e = launch_resample_dst<float>(p, dst_format, s); break;
   }
-  if (lut != nullptr) scratch_free(lut, s);
+  scratch_free(scratch, s);
   count_launch();
   if (e != cudaSuccess) {
     set_error_detail("resample launch: %s", cudaGetErrorString(e));

@@ -85,6 +85,8 @@ int launch_scan_nonfinite(const float* v, int64_t n, int* flag, bool zero, cudaS
 // Returns VKT_OK, an error, or -1 when the tiled kernel does not cover `plan`.
 int launch_filter_tma(const FilterPlan& plan, cudaStream_t s);
 bool tma_supported(const vkt_filter_args& a);
+// The driver entry point for tensor-map encoding is available.
+bool tma_encode_available();
 // Output planes per CTA chunk the tiled kernel would use for `plan`.
 int tma_chunk_planes(const FilterPlan& plan);
 

@@ -93,12 +93,13 @@ struct Shape {
   static constexpr int R = K / 2;
   // u8/u16 5^3: 5 rows (24 x-sum rows = 3 full producer rounds; 1.42 ->
   // 1.26-1.28 ms); f32 5^3 keeps 4 (its raw ring would drop to 3 stages)
-  static constexpr int YPT = K == 3 ? 8 : K == 9 ? 3 : K == 5 && BPC < 4 ? 5 : 4;
+  static constexpr int YPT = K == 3 ? 8 : K == 9 || K == 11 ? 3 : K >= 13 ? 2 : K == 5 && BPC < 4 ? 5 : 4;
+  static constexpr int HQ = (R + 3) / 4;      // halo quads per side of an x-pass item
   static constexpr int RG = 4;
   // 6 producer warps where the x pass is long per consumer row: 3^3 (34 x-sum
   // rows for 32 outputs; u8 0.93 -> 0.89 ms) and 9^3 (20 rows for 12; u16
   // 2.44 -> 2.28 ms); 5^3 / 7^3 measured equal or slower
-  static constexpr int PW = K == 3 || K == 9 ? 6 : 4;
+  static constexpr int PW = K == 3 || K == 9 || K >= 13 ? 6 : 4;
   static constexpr int CTAS = 2;
   static constexpr int CW = 2 * RG;
   static constexpr int THREADS = 32 * (CW + PW);
@@ -109,9 +110,16 @@ struct Shape {
   static constexpr int QPT = (NQ + PT - 1) / PT;
 };
 
+// Extents the separable kernel is built for: odd K = 3 .. MAX_K (gaussian_kernel's
+// default size reaches 11 at sigma 2.5, 13 at 3, 15 at 3.5)
+constexpr int MAX_K = 15;
 __host__ __device__ constexpr int tile_rows(int k, int bpc) {
-  return bpc == 4 ? (k == 3 ? Shape<3, 4>::TY : k == 5 ? Shape<5, 4>::TY : k == 7 ? Shape<7, 4>::TY : Shape<9, 4>::TY)
-                  : (k == 3 ? Shape<3, 2>::TY : k == 5 ? Shape<5, 2>::TY : k == 7 ? Shape<7, 2>::TY : Shape<9, 2>::TY);
+  return bpc == 4 ? (k == 3 ? Shape<3, 4>::TY : k == 5 ? Shape<5, 4>::TY : k == 7 ? Shape<7, 4>::TY
+                     : k == 9 ? Shape<9, 4>::TY : k == 11 ? Shape<11, 4>::TY : k == 13 ? Shape<13, 4>::TY
+                     : Shape<15, 4>::TY)
+                  : (k == 3 ? Shape<3, 2>::TY : k == 5 ? Shape<5, 2>::TY : k == 7 ? Shape<7, 2>::TY
+                     : k == 9 ? Shape<9, 2>::TY : k == 11 ? Shape<11, 2>::TY : k == 13 ? Shape<13, 2>::TY
+                     : Shape<15, 2>::TY);
 }
 __host__ __device__ constexpr int ctas_per_sm(int) { return 2; }
 
@@ -286,7 +294,8 @@ __global__ void __launch_bounds__(Shape<K, (int)sizeof(T)>::THREADS, Shape<K, (i
     const int g = pt & (GPR - 1);
     const int row0 = pt / GPR;
     const int b = (g >> 2) & 1;
-    const int src_off = row0 * C::BX + (C::A - 4) + 4 * g;    // + k * (PT/GPR) * BX
+    constexpr int HQ = S::HQ;
+    const int src_off = row0 * C::BX + (C::A - 4 * HQ) + 4 * g;    // + k * (PT/GPR) * BX
     const int dst_off0 = row0 * HALF + 2 * ((2 * g) ^ b);       // in pairs, + k * (PT/GPR) * HALF
     const int dst_off1 = row0 * HALF + 2 * ((2 * g + 1) ^ b);
     const uint64_t zero2 = tma::f2pack(0.0f, 0.0f);
@@ -324,18 +333,18 @@ __global__ void __launch_bounds__(Shape<K, (int)sizeof(T)>::THREADS, Shape<K, (i
 #pragma unroll
       for (int k = 0; k < S::QPT; ++k) {
         if (S::NQ % PT != 0 && k == S::QPT - 1 && pt + PT * k >= S::NQ) break;
-        // cells x0-4+4g .. x0+4g+7 (and +HALF): output pair jj at tap dx
-        // reads cell 4g + jj + dx - R, i.e. index jj + dx + 4 - R here
+        // cells x0-4HQ+4g .. x0+4g+3+4HQ (and +HALF): output pair jj at tap
+        // dx reads cell 4g + jj + dx - R, i.e. index jj + dx + 4HQ - R here
         const T* src = raw + src_off + k * (PT / GPR) * C::BX;
-        uint64_t P[12];
+        uint64_t P[4 * (2 * HQ + 1)];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < 2 * HQ + 1; ++i) {
           uint32_t lo[4], hi[4];
           tma::load_quad<T>(src + 4 * i, lo);
           tma::load_quad<T>(src + 4 * i + HALF, hi);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            if (4 * i + e < 4 - R || 4 * i + e >= 8 + R) continue;
+            if (4 * i + e < 4 * HQ - R || 4 * i + e >= 4 * HQ + 4 + R) continue;
             if constexpr (sizeof(T) == 4)
               P[4 * i + e] = (uint64_t)lo[e] | ((uint64_t)hi[e] << 32);
             else
@@ -345,9 +354,9 @@ __global__ void __launch_bounds__(Shape<K, (int)sizeof(T)>::THREADS, Shape<K, (i
         uint64_t o[4];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-          o[jj] = tma::ffma2_from(P[jj + 4 - R], f.wx[0], zero2);
+          o[jj] = tma::ffma2_from(P[jj + 4 * HQ - R], f.wx[0], zero2);
 #pragma unroll
-          for (int dx = 1; dx < K; ++dx) tma::ffma2_bw(P[jj + dx + 4 - R], f.wx[dx], o[jj]);
+          for (int dx = 1; dx < K; ++dx) tma::ffma2_bw(P[jj + dx + 4 * HQ - R], f.wx[dx], o[jj]);
         }
         uint64_t* d = xb + k * (PT / GPR) * HALF;
         *reinterpret_cast<uint4*>(d + dst_off0) =
@@ -489,7 +498,7 @@ cudaError_t launch_sep_kernel(const CUtensorMap& ms, const CUtensorMap& ml, cons
   return cudaGetLastError();
 }
 
-// K in {3, 5, 7, 9} x the four address modes, for one voxel format
+// odd K in [3, MAX_K] x the four address modes, for one voxel format
 // (instantiated in filter_sep_{u8,u16,f32}.cu).
 template <typename T>
 cudaError_t launch_sep_dtype(int k, int mode, const CUtensorMap& ms, const CUtensorMap& ml,
@@ -509,6 +518,9 @@ cudaError_t launch_sep_dtype(int k, int mode, const CUtensorMap& ms, const CUten
   VKT_SEP_CASES(5)
   VKT_SEP_CASES(7)
   VKT_SEP_CASES(9)
+  VKT_SEP_CASES(11)
+  VKT_SEP_CASES(13)
+  VKT_SEP_CASES(15)
 #undef VKT_SEP_CASES
   return cudaErrorInvalidValue;
 }

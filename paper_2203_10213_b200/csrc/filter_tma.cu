@@ -218,6 +218,8 @@ int tma_chunk_planes(const FilterPlan& plan) {
   return zc;
 }
 
+bool tma_encode_available() { return encode_fn() != nullptr; }
+
 bool tma_supported(const vkt_filter_args& a) {
   if (a.flags & (VKT_FLAG_EXACT_F64 | VKT_FLAG_FORCE_DIRECT)) return false;
   const int k = a.kdims.x;

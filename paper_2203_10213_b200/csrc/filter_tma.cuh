@@ -97,12 +97,13 @@ struct Layout {
 // Raw TMA box geometry (shared by the host tensor-map encode and the kernel).
 // TMA needs the innermost box coordinate at a 16-byte multiple (measured with
 // tools/tma_probe.cu), so the box starts A >= R cells left of the tile; it
-// spans at least [x0-4, x0+TX+4), the cells the paired ready rows hold.
+// spans at least [x0-4, x0+TX+4), the cells the paired ready rows hold
+// (R > 4, separable kernels only: [x0-4h, x0+TX+4h), h = ceil(R/4) quads).
 __host__ __device__ constexpr int box_align_left(int r, int bpc) {
   return ((r > 4 ? r : 4) + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
 }
 __host__ __device__ constexpr int box_width(int r, int bpc) {
-  return (box_align_left(r, bpc) + TX + 4 + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
+  return (box_align_left(r, bpc) + TX + 4 * ((r > 4 ? r + 3 : 4) / 4) + 16 / bpc - 1) / (16 / bpc) * (16 / bpc);
 }
 
 template <typename T, int K>

@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "dispatch.h"
+#include "filter_sep.cuh"
 
 namespace vkt {
 
@@ -281,7 +282,7 @@ static bool plan_separable(const FilterPlan& plan, vkt_filter_args& cube, Filter
   const int kx = a->kdims.x, ky = a->kdims.y, kz = a->kdims.z;
   int k = kx > ky ? kx : ky;
   k = k > kz ? k : kz;
-  if (k != 3 && k != 5 && k != 7 && k != 9) return false;
+  if (k < 3 || k > sep::MAX_K) return false;  // odd: validated
   if (a->format == VKT_F32 && k == 3) return false;
   const bool unsharded = a->halo_lo == nullptr && a->halo_hi == nullptr &&
                          (a->global_nz <= 0 || a->global_nz == a->dims.z);
@@ -291,7 +292,7 @@ static bool plan_separable(const FilterPlan& plan, vkt_filter_args& cube, Filter
   cube = *a;
   cube.kdims = vkt_int3{k, k, k};
   cube.weights = nullptr;
-  if (!tma_supported(cube)) return false;
+  if (!tma_encode_available()) return false;
   sp = plan;
   sp.args = &cube;
   sp.path = VKT_PATH_SEPARABLE;

@@ -212,3 +212,25 @@ def test_face_tiles_first_covers_every_tile(monkeypatch, mode, fmt, k):
     assert path == "separable" or (fmt == 3 and k == 3)
     ok, ndiff, dmax = within_contract(got, O.apply_filter(stored, fmt, w, mode, workers=1), fmt, w)
     assert ok, (ndiff, dmax)
+
+
+@pytest.mark.parametrize("fmt", [1, 2, 3])
+@pytest.mark.parametrize("k", [11, 13, 15])
+def test_large_extents(fmt, k):
+    """gaussian_kernel's default extent reaches 11 at sigma 2.5, 13 at 3 and
+    15 at 3.5: those run on the separable kernel too (halos of 2 quads per
+    side), every mode, against the oracle; 17 and up take the direct kernel."""
+    rng = np.random.default_rng(k * 3 + fmt)
+    stored = _stored(rng, fmt, (20, 21, 144))
+    sigma = {11: 2.5, 13: 3.0, 15: 3.5}[k]
+    w = O.gaussian_weights(sigma)
+    assert w.shape == (k, k, k)
+    for mode in MODES:
+        want = O.apply_filter(stored, fmt, w, mode, workers=1)
+        got, path = _run(stored, fmt, w, mode)
+        assert path == "separable"
+        ok, ndiff, dmax = within_contract(got, want, fmt, w)
+        assert ok, (mode, ndiff, dmax)
+    src = vk.StructuredVolume((64, 16, 8), vk.DataFormat.UINT16)
+    dst = vk.StructuredVolume(src.dims, src.format)
+    assert vk.filter_path(dst, src, vk.gaussian_kernel(4.0)) == "direct"  # 17^3

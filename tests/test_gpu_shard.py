@@ -108,6 +108,20 @@ def test_sharded_guarded_f32_sees_nonfinite_halo(mode):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("mode", list(vk.AddressMode))
+@pytest.mark.parametrize("fmt", [vk.DataFormat.UINT16, vk.DataFormat.FLOAT32])
+def test_sharded_separable_large_extent(world, mode, fmt):
+    # gaussian_kernel(3.0) is 13^3: rz = 6 halo planes per side, separable
+    rng = np.random.default_rng(31 + world)
+    host = (rng.random((40, 24, 64), dtype=np.float32) if fmt is vk.DataFormat.FLOAT32 else
+            rng.integers(0, 65536, size=(40, 24, 64), dtype=np.uint16))
+    kern = vk.gaussian_kernel(3.0)
+    want = _unsharded(host, fmt, kern, mode)
+    got = _sharded_run(host, fmt, kern, mode, world)
+    assert np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", list(vk.AddressMode))
 def test_sharded_separable_f32_nonfinite(world, mode):
     # the separable f32 kernel recomputes exactly its Inf / NaN outputs with
     # the dense arithmetic, per launch: an Inf / NaN next to a slab boundary

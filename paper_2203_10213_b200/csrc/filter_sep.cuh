@@ -93,13 +93,14 @@ struct Shape {
   static constexpr int R = K / 2;
   // u8/u16 5^3: 5 rows (24 x-sum rows = 3 full producer rounds; 1.42 ->
   // 1.26-1.28 ms); f32 5^3 keeps 4 (its raw ring would drop to 3 stages)
-  static constexpr int YPT = K == 3 ? 8 : K == 9 || K == 11 ? 3 : K >= 13 ? 2 : K == 5 && BPC < 4 ? 5 : 4;
+  static constexpr int YPT = K == 3 ? 8 : K == 9 || K == 11 ? 3 : K >= 19 ? 1 : K >= 13 ? 2
+                             : K == 5 && BPC < 4 ? 5 : 4;
   static constexpr int HQ = (R + 3) / 4;      // halo quads per side of an x-pass item
   static constexpr int RG = 4;
   // 6 producer warps where the x pass is long per consumer row: 3^3 (34 x-sum
   // rows for 32 outputs; u8 0.93 -> 0.89 ms) and 9^3 (20 rows for 12; u16
   // 2.44 -> 2.28 ms); 5^3 / 7^3 measured equal or slower
-  static constexpr int PW = K == 3 || K == 9 || K >= 13 ? 6 : 4;
+  static constexpr int PW = K == 3 || K == 9 || K == 13 || K == 15 || K >= 19 ? 6 : 4;
   static constexpr int CTAS = 2;
   static constexpr int CW = 2 * RG;
   static constexpr int THREADS = 32 * (CW + PW);
@@ -111,16 +112,16 @@ struct Shape {
 };
 
 // Extents the separable kernel is built for: odd K = 3 .. MAX_K (gaussian_kernel's
-// default size reaches 11 at sigma 2.5, 13 at 3, 15 at 3.5)
-constexpr int MAX_K = 15;
-__host__ __device__ constexpr int tile_rows(int k, int bpc) {
-  return bpc == 4 ? (k == 3 ? Shape<3, 4>::TY : k == 5 ? Shape<5, 4>::TY : k == 7 ? Shape<7, 4>::TY
-                     : k == 9 ? Shape<9, 4>::TY : k == 11 ? Shape<11, 4>::TY : k == 13 ? Shape<13, 4>::TY
-                     : Shape<15, 4>::TY)
-                  : (k == 3 ? Shape<3, 2>::TY : k == 5 ? Shape<5, 2>::TY : k == 7 ? Shape<7, 2>::TY
-                     : k == 9 ? Shape<9, 2>::TY : k == 11 ? Shape<11, 2>::TY : k == 13 ? Shape<13, 2>::TY
-                     : Shape<15, 2>::TY);
+// default size reaches 11 at sigma 2.5, 13 at 3, 15 at 3.5, 17 at 4, 21 at 5)
+constexpr int MAX_K = 21;
+template <int BPC>
+__host__ __device__ constexpr int tile_rows_b(int k) {
+  return k == 3 ? Shape<3, BPC>::TY : k == 5 ? Shape<5, BPC>::TY : k == 7 ? Shape<7, BPC>::TY
+       : k == 9 ? Shape<9, BPC>::TY : k == 11 ? Shape<11, BPC>::TY : k == 13 ? Shape<13, BPC>::TY
+       : k == 15 ? Shape<15, BPC>::TY : k == 17 ? Shape<17, BPC>::TY : k == 19 ? Shape<19, BPC>::TY
+       : Shape<21, BPC>::TY;
 }
+__host__ __device__ constexpr int tile_rows(int k, int bpc) { return bpc == 4 ? tile_rows_b<4>(k) : tile_rows_b<2>(k); }
 __host__ __device__ constexpr int ctas_per_sm(int) { return 2; }
 
 // Producer -> consumer handoff of the xb stages on named barriers (hardware
@@ -521,6 +522,9 @@ cudaError_t launch_sep_dtype(int k, int mode, const CUtensorMap& ms, const CUten
   VKT_SEP_CASES(11)
   VKT_SEP_CASES(13)
   VKT_SEP_CASES(15)
+  VKT_SEP_CASES(17)
+  VKT_SEP_CASES(19)
+  VKT_SEP_CASES(21)
 #undef VKT_SEP_CASES
   return cudaErrorInvalidValue;
 }

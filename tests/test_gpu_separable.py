@@ -215,14 +215,15 @@ def test_face_tiles_first_covers_every_tile(monkeypatch, mode, fmt, k):
 
 
 @pytest.mark.parametrize("fmt", [1, 2, 3])
-@pytest.mark.parametrize("k", [11, 13, 15])
+@pytest.mark.parametrize("k", [11, 13, 15, 17, 21])
 def test_large_extents(fmt, k):
-    """gaussian_kernel's default extent reaches 11 at sigma 2.5, 13 at 3 and
-    15 at 3.5: those run on the separable kernel too (halos of 2 quads per
-    side), every mode, against the oracle; 17 and up take the direct kernel."""
+    """gaussian_kernel's default extent reaches 11 at sigma 2.5, 13 at 3, 15 at
+    3.5, 17 at 4 and 21 at 5: those run on the separable kernel too (halos of
+    2-3 quads per side), every mode, against the oracle; 23 and up take the
+    direct kernel."""
     rng = np.random.default_rng(k * 3 + fmt)
-    stored = _stored(rng, fmt, (20, 21, 144))
-    sigma = {11: 2.5, 13: 3.0, 15: 3.5}[k]
+    stored = _stored(rng, fmt, (24, 21, 144))
+    sigma = {11: 2.5, 13: 3.0, 15: 3.5, 17: 4.0, 21: 5.0}[k]
     w = O.gaussian_weights(sigma)
     assert w.shape == (k, k, k)
     for mode in MODES:
@@ -233,4 +234,4 @@ def test_large_extents(fmt, k):
         assert ok, (mode, ndiff, dmax)
     src = vk.StructuredVolume((64, 16, 8), vk.DataFormat.UINT16)
     dst = vk.StructuredVolume(src.dims, src.format)
-    assert vk.filter_path(dst, src, vk.gaussian_kernel(4.0)) == "direct"  # 17^3
+    assert vk.filter_path(dst, src, vk.gaussian_kernel(5.5)) == "direct"  # 23^3

@@ -87,7 +87,9 @@ constexpr int GPR = HALF / 4;  // x-pass items (4 output pairs) per row
 // each cell widened once; consumers x + z from a 72-pair y-sum row): 7^3
 // 1.85 ms, 5^3 1.58, 3^3 1.25, only 9^3 faster (2.17); not adopted.  8-pair
 // x-pass items (14 widened pairs per 8 outputs instead of 2 x 10) with 6
-// producer warps: 7^3 1.57 -> 1.59 ms, f32 7^3 1.86 -> 1.94; not adopted.
+// producer warps: 7^3 1.57 -> 1.59 ms, f32 7^3 1.86 -> 1.94; not adopted.  One
+// TMA store per 2 output planes (half the consumers' store barriers): 7^3
+// 1.576 -> 1.568 ms, f32 slower (the larger staging ring starves the raw ring).
 template <int K, int BPC>
 struct Shape {
   static constexpr int R = K / 2;

@@ -235,3 +235,18 @@ def test_large_extents(fmt, k):
     src = vk.StructuredVolume((64, 16, 8), vk.DataFormat.UINT16)
     dst = vk.StructuredVolume(src.dims, src.format)
     assert vk.filter_path(dst, src, vk.gaussian_kernel(5.5)) == "direct"  # 23^3
+
+
+@pytest.mark.parametrize("fmt", [1, 3])
+def test_large_extent_on_a_tiny_volume(fmt):
+    """21^3 on a 5 x 2 x 3 volume: every tap address-mapped, most of the
+    TMA box outside the volume (the repair table covers it)."""
+    rng = np.random.default_rng(21 + fmt)
+    stored = _stored(rng, fmt, (3, 2, 5))
+    w = O.gaussian_weights(5.0)
+    for mode in MODES:
+        want = O.apply_filter(stored, fmt, w, mode, workers=1)
+        got, path = _run(stored, fmt, w, mode)
+        assert path == "separable"
+        ok, ndiff, dmax = within_contract(got, want, fmt, w)
+        assert ok, (mode, ndiff, dmax)
